@@ -1,0 +1,166 @@
+/*
+ * libfno — C ABI of the B200-native hot path of the model-parallel FNO of
+ * arXiv 2204.01205 (Grady et al.): the 4D (x, y, z, t) spectral-convolution
+ * layer, forward and adjoint, domain-decomposed over x/y.
+ *
+ * Citations are PAPER.md lines ("P:<line>") of /root/reference/PAPER.md.
+ *
+ *   S v   = F^-1 (R_phi . F v)                              P:48-52 (Eq. 3)
+ *   S_dist= F_dist^T (R_phi . F_dist v)
+ *   block : y = sigma(W v + b + S v)                        P:159-169 (Eq. dist_block)
+ *   R_{P->Q} repartition (generalised all-to-all),
+ *            adjoint R_{Q->P}
+ *
+ * Conventions:
+ *   - Fields are NCXYZT, t fastest: float [B][C][Xl][Yl][Z][T], the
+ *     caller's local x/y box (fno_plan_local_box).
+ *   - Retained modes per spatial axis: {0..m-1} ∪ {n-m..n-1} (reading
+ *     Q2), retained index j -> k = j (j < m) else n - 2m + j.  Along t the
+ *     transform is real (rFFT) and keeps {0..mt-1} (readings Q1, Q2).
+ *   - Forward transform unnormalised, inverse scaled by 1/(X Y Z T) (Q3);
+ *     the inverse along t takes the real part with weights c(kt) = 1 at kt=0
+ *     and at the Nyquist kt=T/2, 2 otherwise (real-part semantics, Q4).
+ *   - Spectral weights R (and dR): complex64 (float2 {re, im})
+ *     [C_in][C_out][2mx][2my][kz_hi-kz_lo][mt], the rank's block of retained
+ *     kz planes (fno_plan_owned_modes).  Mixing: W^[o,k] = sum_i V^[i,k] R[i,o,k].
+ *   - Channel weight W: float [C_out][C_in], replicated on every rank
+ *     (broadcast weights); b: float [C] or NULL (= 0).
+ *   - Process grid (1,1,px,py,1,1): rank = ix*py + iy (row-major, Q11).
+ *
+ * Ownership: the library NEVER allocates device memory.  Every data pointer is
+ * device memory on the plan's device, owned by the caller.  The caller also
+ * provides the workspace (fno_plan_workspace_size / fno_plan_set_workspace).
+ * Plans own host metadata and a reference to the communicator only.
+ *
+ * Ordering: every compute call is asynchronous and stream-ordered on `stream`
+ * (a cudaStream_t passed as void*; NULL = legacy default stream).  With P > 1,
+ * every call is collective: all ranks must issue the same sequence of calls.
+ *
+ * Errors: every entry point returns fno_status; it never throws across the
+ * ABI.  Argument errors are detected before any work is enqueued.  CUDA and
+ * NCCL launch errors are returned as FNO_ERR_CUDA / FNO_ERR_NCCL; asynchronous
+ * device faults surface on a later call or at the caller's synchronisation.
+ * fno_last_error() returns a thread-local message naming the failing stage.
+ */
+#ifndef FNO_H_
+#define FNO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FNO_ABI_VERSION 1
+
+typedef enum {
+  FNO_OK = 0,
+  FNO_ERR_INVALID_ARGUMENT = 1, /* bad shape, modes, pointer, partition      */
+  FNO_ERR_PLAN = 2,             /* unplaceable partition / unsupported shape */
+  FNO_ERR_INVALID_STATE = 3,    /* e.g. workspace not set, comm missing      */
+  FNO_ERR_CUDA = 4,             /* a CUDA runtime call or launch failed      */
+  FNO_ERR_NCCL = 5,             /* an NCCL call failed                       */
+  FNO_ERR_WORKSPACE = 6         /* workspace too small or misaligned         */
+} fno_status;
+
+/* flags (fno_problem.flags) */
+#define FNO_ACT_GELU 0u         /* sigma = GELU, exact erf form (default; Q6) */
+#define FNO_ACT_NONE 1u         /* sigma = identity                          */
+
+typedef struct fno_comm_s* fno_comm_t;
+typedef struct fno_plan_s* fno_plan_t;
+
+/* The problem statement of the paper (P:52 modes per dimension, P:182 grid
+ * shape, P:183 width, P:61/P:185 worker partition). */
+typedef struct {
+  int64_t grid[4];   /* global X, Y, Z, T                                     */
+  int32_t batch;     /* B >= 1                                                */
+  int32_t width;     /* C = C_in = C_out >= 1                                 */
+  int32_t modes[4];  /* mx, my, mz (keep {0..m-1} ∪ {n-m..n-1}, 2m <= n);
+                        mt (keep {0..mt-1}, mt <= T/2 + 1)                    */
+  int32_t pgrid[2];  /* px, py: x/y worker grid; z, t undecomposed            */
+  uint32_t flags;    /* FNO_ACT_*                                             */
+} fno_problem;
+
+/* ---- communicator (NCCL over NVLink/NVSwitch) ---------------------------- */
+/* Rank 0 creates the 128-byte unique id; the caller broadcasts it (e.g. with
+ * torch.distributed) and every rank calls fno_comm_init with its rank and the
+ * device it has made current.  Returns FNO_ERR_NCCL on NCCL failure. */
+fno_status fno_comm_unique_id(uint8_t id[128]);
+fno_status fno_comm_init(const uint8_t id[128], int nranks, int rank, fno_comm_t* comm);
+/* A communicator descriptor without a transport: plans built on it answer the
+ * host-side queries (boxes, owned modes, workspace size) for rank `rank` of
+ * `nranks` without any GPU; compute calls on such a plan with P > 1 return
+ * FNO_ERR_INVALID_STATE. */
+fno_status fno_comm_init_local(int nranks, int rank, fno_comm_t* comm);
+fno_status fno_comm_destroy(fno_comm_t comm);
+fno_status fno_comm_size(fno_comm_t comm, int* nranks, int* rank);
+
+/* ---- plan ---------------------------------------------------------------- */
+/* Validates the problem (grid, width > 0; 2m <= n on x, y, z; 1 <= mt <=
+ * T/2+1; px*py == comm size (comm may be NULL iff px*py == 1); X % px == 0 and
+ * Y % py == 0) and derives the local box, the kz ownership block and the
+ * workspace layout.  FNO_ERR_INVALID_ARGUMENT on a bad problem; FNO_ERR_PLAN if
+ * the transform sizes are outside what the kernels support (any length whose
+ * prime factors are 2, 3, 5 up to 1024 per axis). */
+fno_status fno_plan_create(const fno_problem* problem, fno_comm_t comm, fno_plan_t* plan);
+fno_status fno_plan_destroy(fno_plan_t plan);
+/* Bytes of device workspace the caller must provide (256-byte aligned). */
+fno_status fno_plan_workspace_size(fno_plan_t plan, size_t* bytes);
+fno_status fno_plan_set_workspace(fno_plan_t plan, void* dptr, size_t bytes);
+/* Local x/y box of this rank in global coordinates: [lo, hi) per X, Y, Z, T. */
+fno_status fno_plan_local_box(fno_plan_t plan, int64_t lo[4], int64_t hi[4]);
+/* Retained-kz index block [kz_lo, kz_hi) whose weights this rank owns after the
+ * forward exchange (only owners apply R_phi).  May be empty. */
+fno_status fno_plan_owned_modes(fno_plan_t plan, int32_t* kz_lo, int32_t* kz_hi);
+/* Number of complex elements of V^ saved by the forward for the backward:
+ * [B][C][2mx][2my][kz_hi-kz_lo][mt]. */
+fno_status fno_plan_vhat_elems(fno_plan_t plan, size_t* elems);
+
+/* ---- spectral convolution S (Eq. 3 / Eq. sconv_dist) ---------------------- */
+/* u = S v.  v, u: float [B][C][Xl][Yl][Z][T]; R: float2 [C][C][2mx][2my][nkz][mt].
+ * vhat_save (nullable): float2 [B][C][2mx][2my][nkz][mt] receives V^ = F v on
+ * the owned modes. */
+fno_status fno_spectral_conv_fwd(fno_plan_t plan, const float* v, const void* R, float* u,
+                                 void* vhat_save, void* stream);
+/* Adjoint: dv = S^T g (S with R^H[i,o,k] = conj R[o,i,k]) and, if dR != NULL,
+ * the weight gradient dR[i,o,k] (+)= (c(kt)/N) sum_b conj(V^[b,i,k]) G^[b,o,k]
+ * with G^ = F g (requires vhat_saved).  dv may be NULL.  accumulate: 0
+ * overwrites dR, 1 adds into it. */
+fno_status fno_spectral_conv_bwd(fno_plan_t plan, const float* g, const void* R, const void* vhat_saved,
+                                 float* dv, void* dR, int accumulate, void* stream);
+
+/* ---- DFNO block (Eq. dist_block) ----------------------------------------- */
+/* z = W v + b + S v ; y = sigma(z).  z_save, vhat_save nullable (training
+ * mode stores them for fno_layer_bwd). */
+fno_status fno_layer_fwd(fno_plan_t plan, const float* v, const void* R, const float* W, const float* b,
+                         float* y, float* z_save, void* vhat_save, void* stream);
+/* Backward of the block given dy: dz = dy sigma'(z); dv = W^T dz + S^T dz;
+ * dW[o,i] (+)= sum dz[o] v[i]; db[o] (+)= sum dz[o] (both already summed over
+ * all ranks in ascending rank order: the broadcast adjoint);
+ * dR as in fno_spectral_conv_bwd.  db may be NULL. */
+fno_status fno_layer_bwd(fno_plan_t plan, const float* v, const float* z_saved, const void* vhat_saved,
+                         const float* dy, const void* R, const float* W, float* dv, void* dR,
+                         float* dW, float* db, int accumulate, void* stream);
+
+/* ---- repartition R_{P->Q} -------------------------------------- */
+/* Moves a tensor of `ndim` <= 8 dimensions and global shape `global_shape`
+ * from the Cartesian partition src_pgrid to dst_pgrid over the ranks of comm
+ * (row-major ranks, balanced blocks: first n mod p blocks one longer).  Both
+ * partitions must have exactly comm-size workers.  src_local / dst_local are
+ * this rank's boxes (contiguous, row-major, elem_bytes per element).
+ * Workspace: query with workspace == NULL -> *ws_bytes receives the size. The
+ * adjoint is the same call with the pgrids swapped. */
+fno_status fno_repartition(fno_comm_t comm, int ndim, const int64_t* global_shape, const int32_t* src_pgrid,
+                           const int32_t* dst_pgrid, size_t elem_bytes, const void* src_local, void* dst_local,
+                           void* workspace, size_t* ws_bytes, void* stream);
+
+const char* fno_status_string(fno_status s);
+const char* fno_last_error(void);
+int fno_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FNO_H_ */

@@ -1,0 +1,300 @@
+"""B200-native hot path of the model-parallel FNO of arXiv 2204.01205.
+
+Thin Python binding of libfno (include/fno.h).  Argument marshalling only:
+every step of the spectral layer runs in the library's sm_100a kernels and
+NCCL exchanges.  PyTorch supplies device memory, streams and the process
+group used to broadcast the NCCL unique id.  There is no CPU fallback: if
+libfno.so is missing or a call fails, an exception is raised.
+
+Functions keep the ABI names without the ``fno_`` prefix:
+    Problem, Comm, Plan,
+    spectral_conv_fwd, spectral_conv_bwd, layer_fwd, layer_bwd, repartition
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libfno.so")
+
+FNO_ACT_GELU = 0
+FNO_ACT_NONE = 1
+
+_STATUS = {0: "FNO_OK", 1: "FNO_ERR_INVALID_ARGUMENT", 2: "FNO_ERR_PLAN", 3: "FNO_ERR_INVALID_STATE",
+           4: "FNO_ERR_CUDA", 5: "FNO_ERR_NCCL", 6: "FNO_ERR_WORKSPACE"}
+
+
+class FnoError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("grid", ctypes.c_int64 * 4), ("batch", ctypes.c_int32), ("width", ctypes.c_int32),
+                ("modes", ctypes.c_int32 * 4), ("pgrid", ctypes.c_int32 * 2), ("flags", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfno.so (built by paper_2204_01205_b200.build); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(f"{LIB_PATH} not found: run `python -m paper_2204_01205_b200.build` "
+                                    "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+        P = ctypes.POINTER
+        sig = {
+            "fno_comm_unique_id": [ctypes.c_char_p],
+            "fno_comm_init": [ctypes.c_char_p, i32, i32, P(vp)],
+            "fno_comm_init_local": [i32, i32, P(vp)],
+            "fno_comm_destroy": [vp],
+            "fno_comm_size": [vp, P(i32), P(i32)],
+            "fno_plan_create": [P(_Problem), vp, P(vp)],
+            "fno_plan_destroy": [vp],
+            "fno_plan_workspace_size": [vp, P(sz)],
+            "fno_plan_set_workspace": [vp, vp, sz],
+            "fno_plan_local_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
+            "fno_plan_owned_modes": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
+            "fno_plan_vhat_elems": [vp, P(sz)],
+            "fno_spectral_conv_fwd": [vp, vp, vp, vp, vp, vp],
+            "fno_spectral_conv_bwd": [vp, vp, vp, vp, vp, vp, i32, vp],
+            "fno_layer_fwd": [vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "fno_layer_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
+            "fno_repartition": [vp, i32, P(ctypes.c_int64), P(ctypes.c_int32), P(ctypes.c_int32), sz, vp, vp, vp,
+                                P(sz), vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.fno_status_string.argtypes = [ctypes.c_int]
+        L.fno_status_string.restype = ctypes.c_char_p
+        L.fno_last_error.argtypes = []
+        L.fno_last_error.restype = ctypes.c_char_p
+        L.fno_abi_version.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise FnoError(status, where, lib().fno_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+@dataclass
+class Problem:
+    """Problem statement (P:52 modes per dimension, P:182 grid, P:183 width, P:61 partition)."""
+    grid: Sequence[int]                 # global X, Y, Z, T
+    width: int                          # C
+    modes: Sequence[int]                # mx, my, mz, mt
+    batch: int = 1
+    pgrid: Sequence[int] = (1, 1)       # px, py
+    act: str = "gelu"                   # "gelu" | "none"
+
+    def to_c(self) -> _Problem:
+        p = _Problem()
+        for i in range(4):
+            p.grid[i] = int(self.grid[i])
+            p.modes[i] = int(self.modes[i])
+        p.batch = int(self.batch)
+        p.width = int(self.width)
+        p.pgrid[0], p.pgrid[1] = int(self.pgrid[0]), int(self.pgrid[1])
+        p.flags = FNO_ACT_NONE if self.act == "none" else FNO_ACT_GELU
+        return p
+
+
+class Comm:
+    """NCCL communicator of libfno (one process per GPU)."""
+
+    def __init__(self, handle: int, nranks: int, rank: int):
+        self.handle = ctypes.c_void_p(handle)
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().fno_comm_unique_id(buf), "fno_comm_unique_id")
+        return buf.raw
+
+    @classmethod
+    def init(cls, uid: bytes, nranks: int, rank: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(lib().fno_comm_init(uid, nranks, rank, ctypes.byref(h)), "fno_comm_init")
+        return cls(h.value, nranks, rank)
+
+    @classmethod
+    def local(cls, nranks: int, rank: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(lib().fno_comm_init_local(nranks, rank, ctypes.byref(h)), "fno_comm_init_local")
+        return cls(h.value, nranks, rank)
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        """Create on every rank of a torch.distributed group (id broadcast from rank 0)."""
+        import torch
+        import torch.distributed as dist
+        rank, n = dist.get_rank(group), dist.get_world_size(group)
+        uid = cls.unique_id() if rank == 0 else bytes(128)
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        return cls.init(bytes(t.cpu().tolist()), n, rank)
+
+    def destroy(self):
+        if self.handle:
+            lib().fno_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+class Plan:
+    """fno_plan_t plus its caller-owned workspace (a torch uint8 tensor)."""
+
+    def __init__(self, problem: Problem, comm: Optional[Comm] = None, device=None, allocate: bool = True):
+        self.problem = problem
+        self.comm = comm
+        h = ctypes.c_void_p()
+        c = problem.to_c()
+        _check(lib().fno_plan_create(ctypes.byref(c), comm.handle if comm else None, ctypes.byref(h)), "fno_plan_create")
+        self.handle = h
+        self.workspace = None
+        if allocate:
+            import torch
+            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+            self.workspace = torch.empty(max(self.workspace_size(), 256), dtype=torch.uint8, device=dev)
+            _check(lib().fno_plan_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
+                   "fno_plan_set_workspace")
+
+    def workspace_size(self) -> int:
+        n = ctypes.c_size_t()
+        _check(lib().fno_plan_workspace_size(self.handle, ctypes.byref(n)), "fno_plan_workspace_size")
+        return n.value
+
+    def local_box(self):
+        lo = (ctypes.c_int64 * 4)()
+        hi = (ctypes.c_int64 * 4)()
+        _check(lib().fno_plan_local_box(self.handle, lo, hi), "fno_plan_local_box")
+        return list(zip(lo, hi))
+
+    def owned_modes(self):
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().fno_plan_owned_modes(self.handle, ctypes.byref(a), ctypes.byref(b)), "fno_plan_owned_modes")
+        return a.value, b.value
+
+    def vhat_elems(self) -> int:
+        n = ctypes.c_size_t()
+        _check(lib().fno_plan_vhat_elems(self.handle, ctypes.byref(n)), "fno_plan_vhat_elems")
+        return n.value
+
+    def local_shape(self):
+        box = self.local_box()
+        return (self.problem.batch, self.problem.width) + tuple(hi - lo for lo, hi in box)
+
+    def weight_shape(self):
+        lo, hi = self.owned_modes()
+        mx, my, mz, mt = self.problem.modes
+        C = self.problem.width
+        return (C, C, 2 * mx, 2 * my, hi - lo, mt)
+
+    def vhat_shape(self):
+        s = self.weight_shape()
+        return (self.problem.batch,) + s[1:]
+
+    def destroy(self):
+        if self.handle:
+            lib().fno_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def _contig(*ts):
+    for t in ts:
+        if t is not None and not t.is_contiguous():
+            raise ValueError("libfno expects contiguous tensors")
+
+
+def spectral_conv_fwd(plan: Plan, v, R, u, vhat_save=None, stream=None):
+    """u = S v (Eq. 3 / P:121 Eq. sconv_dist)."""
+    _contig(v, R, u, vhat_save)
+    _check(lib().fno_spectral_conv_fwd(plan.handle, _ptr(v), _ptr(R), _ptr(u), _ptr(vhat_save), _stream(stream)),
+           "fno_spectral_conv_fwd")
+
+
+def spectral_conv_bwd(plan: Plan, g, R, vhat_saved=None, dv=None, dR=None, accumulate=False, stream=None):
+    """dv = S^T g and dR (+)= (c/N) sum_b conj(V^) G^."""
+    _contig(g, R, vhat_saved, dv, dR)
+    _check(lib().fno_spectral_conv_bwd(plan.handle, _ptr(g), _ptr(R), _ptr(vhat_saved), _ptr(dv), _ptr(dR),
+                                       int(bool(accumulate)), _stream(stream)), "fno_spectral_conv_bwd")
+
+
+def layer_fwd(plan: Plan, v, R, W, b, y, z_save=None, vhat_save=None, stream=None):
+    """y = sigma(W v + b + S v) (Eq. dist_block)."""
+    _contig(v, R, W, b, y, z_save, vhat_save)
+    _check(lib().fno_layer_fwd(plan.handle, _ptr(v), _ptr(R), _ptr(W), _ptr(b), _ptr(y), _ptr(z_save),
+                               _ptr(vhat_save), _stream(stream)), "fno_layer_fwd")
+
+
+def layer_bwd(plan: Plan, v, z_saved, vhat_saved, dy, R, W, dv, dR, dW, db=None, accumulate=False, stream=None):
+    """Backward of the DFNO block; dW, db summed over all ranks."""
+    _contig(v, z_saved, vhat_saved, dy, R, W, dv, dR, dW, db)
+    _check(lib().fno_layer_bwd(plan.handle, _ptr(v), _ptr(z_saved), _ptr(vhat_saved), _ptr(dy), _ptr(R), _ptr(W),
+                               _ptr(dv), _ptr(dR), _ptr(dW), _ptr(db), int(bool(accumulate)), _stream(stream)),
+           "fno_layer_bwd")
+
+
+def repartition(comm: Optional[Comm], global_shape, src_pgrid, dst_pgrid, src_local, dst_local, stream=None):
+    """R_{P->Q}; the adjoint is the call with the pgrids swapped."""
+    import torch
+    nd = len(global_shape)
+    shp = (ctypes.c_int64 * nd)(*[int(s) for s in global_shape])
+    sp = (ctypes.c_int32 * nd)(*[int(s) for s in src_pgrid])
+    dp = (ctypes.c_int32 * nd)(*[int(s) for s in dst_pgrid])
+    eb = src_local.element_size()
+    n = ctypes.c_size_t(0)
+    h = comm.handle if comm else None
+    _check(lib().fno_repartition(h, nd, shp, sp, dp, eb, None, None, None, ctypes.byref(n), None),
+           "fno_repartition(size)")
+    ws = torch.empty(max(n.value, 256), dtype=torch.uint8, device=src_local.device)
+    n2 = ctypes.c_size_t(ws.numel())
+    _contig(src_local, dst_local)
+    _check(lib().fno_repartition(h, nd, shp, sp, dp, eb, _ptr(src_local), _ptr(dst_local), ws.data_ptr(),
+                                 ctypes.byref(n2), _stream(stream)), "fno_repartition")
+    return ws  # keep alive until the stream has consumed it
+
+
+__all__ = ["Problem", "Comm", "Plan", "FnoError", "lib", "spectral_conv_fwd", "spectral_conv_bwd", "layer_fwd",
+           "layer_bwd", "repartition", "LIB_PATH"]

@@ -1,0 +1,700 @@
+// libfno C ABI: plan / communicator / workspace logic on the host and the
+// stream-ordered orchestration of the kernels and NCCL exchanges.
+//
+// Forward spectral convolution on P = px*py ranks:
+//   pass A (t, z local; I_1)  -> exchange 1 (R_{P_xy -> P_kz})
+//   -> pass B: y fwd, x fwd (I_2), mixing on owned kz, x inv, y inv
+//   -> exchange 2 (R_{P_kz -> P_xy}, the adjoint) -> pass C (z, t inverse
+//   fused with the DFNO block epilogue).
+// Only the retained-mode slab travels: truncation happens before the exchange
+// (reading Q9).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fno.h"
+#include "launch.h"
+
+using namespace fno;
+
+namespace {
+
+thread_local std::string g_err;
+
+fno_status fail(fno_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define FNO_CUDA(call, stage)                                                                        \
+  do {                                                                                               \
+    cudaError_t _e = (call);                                                                         \
+    if (_e != cudaSuccess) return fail(FNO_ERR_CUDA, std::string(stage) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+#define FNO_NCCL(call, stage)                                                                        \
+  do {                                                                                               \
+    ncclResult_t _r = (call);                                                                        \
+    if (_r != ncclSuccess) return fail(FNO_ERR_NCCL, std::string(stage) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+void block_range(long long n, int p, int i, long long* lo, long long* hi) {
+  long long q = n / p, r = n % p;
+  *lo = i * q + std::min<long long>(i, r);
+  *hi = *lo + q + (i < r ? 1 : 0);
+}
+
+// smallest L in the supported list that divides n and is >= need
+template <class Pred>
+int choose_L(long long n, long long need, Pred supported, const std::vector<int>& cands) {
+  int best = 0;
+  for (int L : cands)
+    if (n % L == 0 && L >= need && supported(L) && (best == 0 || L < best)) best = L;
+  return best;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct fno_comm_s {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+struct fno_plan_s {
+  fno_problem pb;
+  fno_comm_t comm = nullptr;
+  int P = 1, rank = 0, px = 1, py = 1, ix = 0, iy = 0;
+  long long X, Y, Z, T, Xl, Yl;
+  int B, C, mx, my, mz, mt;
+  int act_gelu = 1;
+  std::vector<int> kz_lo;  // P+1
+  int nkz = 0;             // own block
+  int LZ, LT, LX, LY;
+  int Qz, Qt, Qx, Qy;
+  int NP;                  // planes per pass-A batch
+  int num_sms = 148;
+  int grid_a = 1, grid_c = 1, grid_c_bwd = 1;
+  size_t smem_a = 0, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
+  long long mloc = 0;      // owned modes: 4 mx my nkz mt
+  // workspace (bytes offsets)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, total;
+  size_t n_slab_xy, n_slab_kz, n_h, n_mode;
+  int max_grid_c = 0;
+};
+
+// ---------------------------------------------------------------------------
+// status / version
+// ---------------------------------------------------------------------------
+extern "C" const char* fno_status_string(fno_status s) {
+  switch (s) {
+    case FNO_OK: return "FNO_OK";
+    case FNO_ERR_INVALID_ARGUMENT: return "FNO_ERR_INVALID_ARGUMENT";
+    case FNO_ERR_PLAN: return "FNO_ERR_PLAN";
+    case FNO_ERR_INVALID_STATE: return "FNO_ERR_INVALID_STATE";
+    case FNO_ERR_CUDA: return "FNO_ERR_CUDA";
+    case FNO_ERR_NCCL: return "FNO_ERR_NCCL";
+    case FNO_ERR_WORKSPACE: return "FNO_ERR_WORKSPACE";
+  }
+  return "FNO_ERR_UNKNOWN";
+}
+extern "C" const char* fno_last_error(void) { return g_err.c_str(); }
+extern "C" int fno_abi_version(void) { return FNO_ABI_VERSION; }
+
+// ---------------------------------------------------------------------------
+// communicator
+// ---------------------------------------------------------------------------
+extern "C" fno_status fno_comm_unique_id(uint8_t id[128]) {
+  if (!id) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_comm_unique_id: id is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  FNO_NCCL(ncclGetUniqueId(&u), "ncclGetUniqueId");
+  std::memcpy(id, &u, 128);
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_comm_init(const uint8_t id[128], int nranks, int rank, fno_comm_t* comm) {
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_comm_init: bad arguments");
+  auto* c = new fno_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(FNO_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *comm = c;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_comm_init_local(int nranks, int rank, fno_comm_t* comm) {
+  if (!comm || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_comm_init_local: bad arguments");
+  auto* c = new fno_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  *comm = c;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_comm_destroy(fno_comm_t comm) {
+  if (!comm) return FNO_OK;
+  if (comm->nccl) ncclCommDestroy(comm->nccl);
+  delete comm;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_comm_size(fno_comm_t comm, int* nranks, int* rank) {
+  if (!comm || !nranks || !rank) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_comm_size: NULL argument");
+  *nranks = comm->nranks;
+  *rank = comm->rank;
+  return FNO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fno_plan_t* out) {
+  if (!pb || !out) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: NULL argument");
+  for (int d = 0; d < 4; ++d)
+    if (pb->grid[d] <= 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: grid extents must be > 0");
+  if (pb->batch < 1 || pb->width < 1) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: batch and width must be >= 1");
+  for (int d = 0; d < 3; ++d)
+    if (pb->modes[d] < 1 || 2LL * pb->modes[d] > pb->grid[d])
+      return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: spatial modes need 1 <= m and 2m <= n (P:52, reading Q2)");
+  if (pb->modes[3] < 1 || pb->modes[3] > pb->grid[3] / 2 + 1)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: time modes need 1 <= mt <= T/2+1 (reading Q2)");
+  if (pb->pgrid[0] < 1 || pb->pgrid[1] < 1) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: pgrid entries must be >= 1");
+  if (pb->flags & ~1u) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: unknown flags");
+  const int P = pb->pgrid[0] * pb->pgrid[1];
+  if (P > FNO_MAXP) return fail(FNO_ERR_PLAN, "fno_plan_create: more than 64 ranks");
+  int nranks = 1, rank = 0;
+  if (comm) { nranks = comm->nranks; rank = comm->rank; }
+  if (nranks != P) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: px*py must equal the communicator size (NULL comm => 1)");
+  if (pb->grid[0] % pb->pgrid[0] || pb->grid[1] % pb->pgrid[1])
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: X % px and Y % py must be 0 (balanced uneven boxes are not supported yet)");
+  if (2 * pb->modes[2] > 32767) return fail(FNO_ERR_PLAN, "fno_plan_create: too many z modes");
+
+  auto* p = new fno_plan_s();
+  p->pb = *pb;
+  p->comm = comm;
+  p->P = P;
+  p->rank = rank;
+  p->px = pb->pgrid[0];
+  p->py = pb->pgrid[1];
+  p->ix = rank / p->py;
+  p->iy = rank % p->py;
+  p->X = pb->grid[0]; p->Y = pb->grid[1]; p->Z = pb->grid[2]; p->T = pb->grid[3];
+  p->Xl = p->X / p->px; p->Yl = p->Y / p->py;
+  p->B = pb->batch; p->C = pb->width;
+  p->mx = pb->modes[0]; p->my = pb->modes[1]; p->mz = pb->modes[2]; p->mt = pb->modes[3];
+  p->act_gelu = (pb->flags & FNO_ACT_NONE) ? 0 : 1;
+  p->kz_lo.resize(P + 1);
+  for (int d = 0; d < P; ++d) {
+    long long lo, hi;
+    block_range(2LL * p->mz, P, d, &lo, &hi);
+    p->kz_lo[d] = int(lo);
+    p->kz_lo[d + 1] = int(hi);
+  }
+  p->nkz = p->kz_lo[rank + 1] - p->kz_lo[rank];
+
+  // transform sizes (readings: z real input needs kz' = 0..mz; t needs
+  // min(2mt-1, T) residues; x, y need 2m residues)
+  const std::vector<int> ac_z = {2, 4, 8, 16, 32};
+  const std::vector<int> ac_t = {4, 5, 8, 15, 16, 30, 32};
+  const std::vector<int> bs = {2, 4, 5, 6, 8, 16, 30, 32};
+  const long long need_t = std::min<long long>(2LL * p->mt - 1, p->T);
+  p->LZ = 0; p->LT = 0;
+  for (int lz : ac_z) {
+    if (p->Z % lz || lz < p->mz + 1) continue;
+    for (int lt : ac_t) {
+      if (p->T % lt || lt < need_t || !ac_pair_supported(lz, lt)) continue;
+      if (p->LZ == 0 || lz < p->LZ || (lz == p->LZ && lt < p->LT)) { p->LZ = lz; p->LT = lt; }
+    }
+  }
+  p->LX = choose_L(p->X, 2LL * p->mx, b_size_supported, bs);
+  p->LY = choose_L(p->Y, 2LL * p->my, b_size_supported, bs);
+  if (!p->LZ || !p->LT || !p->LX || !p->LY) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "fno_plan_create: no instantiated register-FFT size for grid (%lld,%lld,%lld,%lld) modes (%d,%d,%d,%d)",
+                  p->X, p->Y, p->Z, p->T, p->mx, p->my, p->mz, p->mt);
+    delete p;
+    return fail(FNO_ERR_PLAN, buf);
+  }
+  p->Qz = int(p->Z / p->LZ); p->Qt = int(p->T / p->LT);
+  p->Qx = int(p->X / p->LX); p->Qy = int(p->Y / p->LY);
+
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0) p->num_sms = sms;
+  } else {
+    cudaGetLastError();
+  }
+
+  // pass A batching: ~256 pencils and <= 48 KB of staged planes per batch
+  const long long ZT = p->Z * p->T;
+  p->NP = int(std::max<long long>(1, std::min<long long>(256 / p->T, (48 * 1024) / (ZT * 4))));
+  p->smem_a = pass_a_smem(int(p->Z), int(p->T), p->mz, p->NP);
+  p->smem_c_u = pass_c_smem(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_U);
+  p->smem_c_fwd = pass_c_smem(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD);
+  p->smem_c_bwd = pass_c_smem(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD);
+  const size_t smem_max = 227 * 1024;
+  if (p->smem_a > smem_max || p->smem_c_bwd > smem_max) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "fno_plan_create: shared memory per CTA too large (pass A %zu, pass C %zu bytes)", p->smem_a, p->smem_c_bwd);
+    delete p;
+    return fail(FNO_ERR_PLAN, buf);
+  }
+  const long long n_planes = (long long)p->B * p->C * p->Xl * p->Yl;
+  const long long n_batches = (n_planes + p->NP - 1) / p->NP;
+  const int per_sm_a = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (p->smem_a + 1024))));
+  p->grid_a = int(std::max<long long>(1, std::min<long long>(n_batches, (long long)p->num_sms * per_sm_a)));
+  const long long n_cols = (long long)p->B * p->Xl * p->Yl;
+  auto grid_for = [&](size_t smem) {
+    const int per_sm = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (smem + 1024))));
+    return int(std::max<long long>(1, std::min<long long>(n_cols, (long long)p->num_sms * per_sm)));
+  };
+  p->grid_c = grid_for(p->smem_c_fwd);
+  p->grid_c_bwd = grid_for(p->smem_c_bwd);
+  p->max_grid_c = p->grid_c_bwd;
+
+  // workspace layout
+  p->mloc = 4LL * p->mx * p->my * p->nkz * p->mt;
+  p->n_slab_xy = size_t(p->B) * p->Xl * p->Yl * p->C * 2 * p->mz * p->mt;
+  p->n_slab_kz = size_t(P) * p->B * p->Xl * p->Yl * p->C * p->nkz * p->mt;
+  p->n_h = size_t(p->B) * p->nkz * p->C * p->X * 2 * p->my * p->mt;
+  p->n_mode = size_t(p->B) * p->C * p->mloc;
+  const size_t dwlen = size_t(p->C) * p->C + p->C;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  p->o_slab_xy = take(p->n_slab_xy * 8);
+  p->o_slab_kz = (P == 1) ? p->o_slab_xy : take(p->n_slab_kz * 8);
+  p->o_h = take(p->n_h * 8);
+  p->o_vhat = take(p->n_mode * 8);
+  p->o_what = take(p->n_mode * 8);
+  p->o_ghat = take(p->n_mode * 8);
+  p->o_dwpart = take(size_t(p->max_grid_c) * dwlen * 4);
+  p->o_dwloc = take(dwlen * 4);
+  p->o_dwall = take(size_t(P) * dwlen * 4);
+  p->total = off;
+  *out = p;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_destroy(fno_plan_t p) {
+  delete p;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_workspace_size(fno_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_workspace_size: NULL argument");
+  *bytes = p->total;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_set_workspace(fno_plan_t p, void* dptr, size_t bytes) {
+  if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_workspace: NULL plan");
+  if (!dptr || bytes < p->total) return fail(FNO_ERR_WORKSPACE, "fno_plan_set_workspace: workspace NULL or smaller than fno_plan_workspace_size");
+  if (reinterpret_cast<uintptr_t>(dptr) & 255) return fail(FNO_ERR_WORKSPACE, "fno_plan_set_workspace: workspace must be 256-byte aligned");
+  p->ws = dptr;
+  p->ws_bytes = bytes;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_local_box(fno_plan_t p, int64_t lo[4], int64_t hi[4]) {
+  if (!p || !lo || !hi) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_local_box: NULL argument");
+  lo[0] = p->ix * p->Xl; hi[0] = lo[0] + p->Xl;
+  lo[1] = p->iy * p->Yl; hi[1] = lo[1] + p->Yl;
+  lo[2] = 0; hi[2] = p->Z;
+  lo[3] = 0; hi[3] = p->T;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_owned_modes(fno_plan_t p, int32_t* kz_lo, int32_t* kz_hi) {
+  if (!p || !kz_lo || !kz_hi) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_owned_modes: NULL argument");
+  *kz_lo = p->kz_lo[p->rank];
+  *kz_hi = p->kz_lo[p->rank + 1];
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_vhat_elems(fno_plan_t p, size_t* elems) {
+  if (!p || !elems) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_vhat_elems: NULL argument");
+  *elems = p->n_mode;
+  return FNO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// orchestration
+// ---------------------------------------------------------------------------
+namespace {
+
+template <class T>
+T* wsp(fno_plan_t p, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(p->ws) + off);
+}
+
+KzSlab make_kzslab(fno_plan_t p) {
+  KzSlab s{};
+  s.P = p->P;
+  long long off = 0;
+  const long long per = (long long)p->B * p->Xl * p->Yl * p->C * p->mt;
+  for (int d = 0; d <= p->P; ++d) s.kz_lo[d] = p->kz_lo[d];
+  for (int d = 0; d < p->P; ++d) {
+    s.off[d] = off;
+    off += per * (p->kz_lo[d + 1] - p->kz_lo[d]);
+  }
+  return s;
+}
+
+PassBParams make_b(fno_plan_t p, const float2* in, float2* out, int Q) {
+  PassBParams b{};
+  b.in = in; b.out = out;
+  b.B = p->B; b.C = p->C; b.X = int(p->X); b.Y = int(p->Y); b.Xl = int(p->Xl); b.Yl = int(p->Yl);
+  b.py = p->py; b.nkz = p->nkz; b.mt = p->mt; b.mx = p->mx; b.my = p->my; b.Q = Q;
+  b.chunk = (long long)p->B * p->Xl * p->Yl * p->C * p->nkz * p->mt;
+  return b;
+}
+
+// exchange 1 (forward): kz-owner ordered send buffer -> x/y-source ordered receive buffer
+fno_status exchange_fwd(fno_plan_t p, cudaStream_t st) {
+  if (p->P == 1) return FNO_OK;
+  const KzSlab s = make_kzslab(p);
+  const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;  // complex per kz plane
+  float2* send = wsp<float2>(p, p->o_slab_xy);
+  float2* recv = wsp<float2>(p, p->o_slab_kz);
+  FNO_NCCL(ncclGroupStart(), "exchange 1: ncclGroupStart");
+  for (int d = 0; d < p->P; ++d) {
+    const size_t ns = per * (p->kz_lo[d + 1] - p->kz_lo[d]);
+    const size_t nr = per * p->nkz;
+    if (ns) FNO_NCCL(ncclSend(send + s.off[d], 2 * ns, ncclFloat, d, p->comm->nccl, st), "exchange 1: ncclSend");
+    if (nr) FNO_NCCL(ncclRecv(recv + d * nr, 2 * nr, ncclFloat, d, p->comm->nccl, st), "exchange 1: ncclRecv");
+  }
+  FNO_NCCL(ncclGroupEnd(), "exchange 1: ncclGroupEnd");
+  return FNO_OK;
+}
+
+// exchange 2 (adjoint): x/y-destination ordered -> kz-owner ordered
+fno_status exchange_bwd(fno_plan_t p, cudaStream_t st) {
+  if (p->P == 1) return FNO_OK;
+  const KzSlab s = make_kzslab(p);
+  const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;
+  float2* send = wsp<float2>(p, p->o_slab_kz);
+  float2* recv = wsp<float2>(p, p->o_slab_xy);
+  FNO_NCCL(ncclGroupStart(), "exchange 2: ncclGroupStart");
+  for (int d = 0; d < p->P; ++d) {
+    const size_t ns = per * p->nkz;
+    const size_t nr = per * (p->kz_lo[d + 1] - p->kz_lo[d]);
+    if (ns) FNO_NCCL(ncclSend(send + d * ns, 2 * ns, ncclFloat, d, p->comm->nccl, st), "exchange 2: ncclSend");
+    if (nr) FNO_NCCL(ncclRecv(recv + s.off[d], 2 * nr, ncclFloat, d, p->comm->nccl, st), "exchange 2: ncclRecv");
+  }
+  FNO_NCCL(ncclGroupEnd(), "exchange 2: ncclGroupEnd");
+  return FNO_OK;
+}
+
+fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode, cudaStream_t st) {
+  PassAParams a{};
+  a.in0 = in0; a.in1 = in1;
+  a.out = wsp<float2>(p, p->o_slab_xy);
+  a.n_planes = (long long)p->B * p->C * p->Xl * p->Yl;
+  a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->NP;
+  a.C = p->C; a.Xl = int(p->Xl); a.Yl = int(p->Yl);
+  a.slab = make_kzslab(p);
+  FNO_CUDA(launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a, p->smem_a, st), "pass A");
+  return FNO_OK;
+}
+
+// pass B forward half: slab (kz block, x/y-source ordered) -> V^ (owned modes)
+fno_status run_b_fwd(fno_plan_t p, float2* vhat_out, cudaStream_t st) {
+  if (p->nkz == 0) return FNO_OK;
+  float2* slab = wsp<float2>(p, p->o_slab_kz);
+  float2* H = wsp<float2>(p, p->o_h);
+  FNO_CUDA(launch_b_yfwd(make_b(p, slab, H, p->Qy), p->LY, st), "pass B y-forward");
+  FNO_CUDA(launch_b_xfwd(make_b(p, H, vhat_out, p->Qx), p->LX, st), "pass B x-forward");
+  return FNO_OK;
+}
+
+// pass B inverse half: W^ -> slab (x/y-destination ordered)
+fno_status run_b_inv(fno_plan_t p, const float2* what, cudaStream_t st) {
+  if (p->nkz == 0) return FNO_OK;
+  float2* slab = wsp<float2>(p, p->o_slab_kz);
+  float2* H = wsp<float2>(p, p->o_h);
+  FNO_CUDA(launch_b_xinv(make_b(p, what, H, p->Qx), p->LX, st), "pass B x-inverse");
+  FNO_CUDA(launch_b_yinv(make_b(p, H, slab, p->Qy), p->LY, st), "pass B y-inverse");
+  return FNO_OK;
+}
+
+MixParams make_mix(fno_plan_t p) {
+  MixParams m{};
+  m.M = p->mloc; m.B = p->B; m.C = p->C; m.mt = p->mt; m.T = int(p->T);
+  m.inv_n = float(1.0 / (double(p->X) * p->Y * p->Z * p->T));
+  return m;
+}
+
+PassCParams make_c(fno_plan_t p) {
+  PassCParams c{};
+  c.in = wsp<float2>(p, p->o_slab_xy);
+  c.n_cols = (long long)p->B * p->Xl * p->Yl;
+  c.B = p->B; c.C = p->C; c.Xl = int(p->Xl); c.Yl = int(p->Yl); c.Z = int(p->Z); c.T = int(p->T);
+  c.mz = p->mz; c.mt = p->mt; c.Qz = p->Qz; c.Qt = p->Qt;
+  c.act_gelu = p->act_gelu;
+  c.inv_n = float(1.0 / (double(p->X) * p->Y * p->Z * p->T));
+  c.slab = make_kzslab(p);
+  return c;
+}
+
+fno_status check_ready(fno_plan_t p, const char* who) {
+  if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": NULL plan");
+  if (!p->ws) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": workspace not set (fno_plan_set_workspace)");
+  if (p->P > 1 && (!p->comm || !p->comm->nccl)) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": communicator missing");
+  return FNO_OK;
+}
+
+#define FNO_TRY(x)                \
+  do {                            \
+    fno_status _s = (x);          \
+    if (_s != FNO_OK) return _s;  \
+  } while (0)
+
+// forward spectral chain up to the second exchange; the slab for pass C is
+// left in the x/y-ordered buffer.  vhat: where V^ goes (scratch or saved).
+fno_status spectral_fwd_to_slab(fno_plan_t p, const float* v, const float2* R, float2* vhat, cudaStream_t st) {
+  FNO_TRY(run_pass_a(p, v, nullptr, MODE_V, st));
+  FNO_TRY(exchange_fwd(p, st));
+  FNO_TRY(run_b_fwd(p, vhat, st));
+  if (p->nkz > 0) {
+    MixParams m = make_mix(p);
+    m.vhat = vhat; m.R = R; m.what = wsp<float2>(p, p->o_what);
+    FNO_CUDA(launch_mix_fwd(m, st), "mixing (forward)");
+  }
+  FNO_TRY(run_b_inv(p, wsp<float2>(p, p->o_what), st));
+  FNO_TRY(exchange_bwd(p, st));
+  return FNO_OK;
+}
+
+// adjoint spectral chain on g (input already in the pass-A form selected by mode)
+fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1, int mode, const float2* R,
+                                const float2* vhat_saved, float2* dR, int accumulate, cudaStream_t st) {
+  FNO_TRY(run_pass_a(p, in0, in1, mode, st));
+  FNO_TRY(exchange_fwd(p, st));
+  float2* ghat = wsp<float2>(p, p->o_ghat);
+  FNO_TRY(run_b_fwd(p, ghat, st));
+  if (p->nkz > 0) {
+    MixParams m = make_mix(p);
+    m.vhat = vhat_saved; m.R = R; m.ghat = ghat; m.what = wsp<float2>(p, p->o_what);
+    m.dR = dR; m.accumulate = accumulate;
+    FNO_CUDA(launch_mix_bwd(m, st), "mixing (backward)");
+  }
+  FNO_TRY(run_b_inv(p, wsp<float2>(p, p->o_what), st));
+  FNO_TRY(exchange_bwd(p, st));
+  return FNO_OK;
+}
+
+}  // namespace
+
+extern "C" fno_status fno_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
+                                            void* stream) {
+  FNO_TRY(check_ready(p, "fno_spectral_conv_fwd"));
+  if (!v || !u || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_fwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
+  FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
+  PassCParams c = make_c(p);
+  c.out = u;
+  FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (u)");
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
+                                            float* dv, void* dR, int accumulate, void* stream) {
+  FNO_TRY(check_ready(p, "fno_spectral_conv_bwd"));
+  if (!g || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: NULL g or R");
+  if (dR && !vhat_saved && p->nkz > 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: dR requires vhat_saved");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FNO_TRY(spectral_bwd_to_slab(p, g, nullptr, MODE_V, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
+                               static_cast<float2*>(dR), accumulate, st));
+  if (dv) {
+    PassCParams c = make_c(p);
+    c.out = dv;
+    FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (adjoint u)");
+  }
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
+                                    float* z_save, void* vhat_save, void* stream) {
+  FNO_TRY(check_ready(p, "fno_layer_fwd"));
+  if (!v || !W || !y || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_fwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
+  FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
+  PassCParams c = make_c(p);
+  c.v = v; c.W = W; c.bias = b; c.out = y; c.zsave = z_save;
+  FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z_saved, const void* vhat_saved,
+                                    const float* dy, const void* R, const float* W, float* dv, void* dR, float* dW,
+                                    float* db, int accumulate, void* stream) {
+  FNO_TRY(check_ready(p, "fno_layer_bwd"));
+  if (!v || !dy || !W || !dv || !dW || (!R && p->nkz > 0) || (p->act_gelu && !z_saved))
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_bwd: NULL data pointer (v, dy, W, dv, dW, R and z_saved for GELU are required)");
+  if (dR && !vhat_saved && p->nkz > 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_bwd: dR requires vhat_saved");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int mode = p->act_gelu ? MODE_DZ_GELU : MODE_DZ_NONE;
+  FNO_TRY(spectral_bwd_to_slab(p, dy, z_saved, mode, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
+                               static_cast<float2*>(dR), accumulate, st));
+  PassCParams c = make_c(p);
+  c.v = v; c.dy = dy; c.zs = z_saved; c.W = W; c.out = dv;
+  c.dWpart = wsp<float>(p, p->o_dwpart);
+  FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
+  const int len = p->C * p->C + p->C;
+  if (p->P == 1) {
+    FNO_CUDA(launch_rowsum(c.dWpart, p->grid_c_bwd, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
+  } else {
+    float* loc = wsp<float>(p, p->o_dwloc);
+    float* all = wsp<float>(p, p->o_dwall);
+    FNO_CUDA(launch_rowsum(c.dWpart, p->grid_c_bwd, len, len, loc, nullptr, 0, st), "dW/db local reduction");
+    FNO_NCCL(ncclAllGather(loc, all, size_t(len), ncclFloat, p->comm->nccl, st), "dW/db all-gather");
+    FNO_CUDA(launch_rowsum(all, p->P, len, p->C * p->C, dW, db, accumulate, st), "dW/db rank-ordered sum");
+  }
+  return FNO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// general repartition R_{P->Q}
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Box {
+  long long lo[8], hi[8];
+};
+
+Box box_of(int ndim, const int64_t* shape, const int32_t* pg, int rank) {
+  Box b{};
+  int coords[8];
+  int r = rank;
+  for (int d = ndim - 1; d >= 0; --d) {
+    coords[d] = r % pg[d];
+    r /= pg[d];
+  }
+  for (int d = 0; d < ndim; ++d) block_range(shape[d], pg[d], coords[d], &b.lo[d], &b.hi[d]);
+  return b;
+}
+
+bool intersect(int ndim, const Box& a, const Box& b, Box* o) {
+  for (int d = 0; d < ndim; ++d) {
+    o->lo[d] = std::max(a.lo[d], b.lo[d]);
+    o->hi[d] = std::min(a.hi[d], b.hi[d]);
+    if (o->lo[d] >= o->hi[d]) return false;
+  }
+  return true;
+}
+
+long long box_elems(int ndim, const Box& b) {
+  long long n = 1;
+  for (int d = 0; d < ndim; ++d) n *= (b.hi[d] - b.lo[d]);
+  return n;
+}
+
+}  // namespace
+
+cudaError_t launch_box_copy(const void* src, const long long* src_ext, const long long* src_lo, void* dst,
+                            const long long* dst_ext, const long long* dst_lo, const long long* cnt, int ndim,
+                            size_t elem_bytes, cudaStream_t st);
+
+extern "C" fno_status fno_repartition(fno_comm_t comm, int ndim, const int64_t* shape, const int32_t* src_pg,
+                                      const int32_t* dst_pg, size_t elem_bytes, const void* src_local, void* dst_local,
+                                      void* workspace, size_t* ws_bytes, void* stream) {
+  if (ndim < 1 || ndim > 8 || !shape || !src_pg || !dst_pg || !ws_bytes || elem_bytes == 0)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_repartition: bad arguments (1 <= ndim <= 8, non-NULL shape/pgrids/ws_bytes)");
+  int nranks = 1, rank = 0;
+  if (comm) { nranks = comm->nranks; rank = comm->rank; }
+  long long ns = 1, nd = 1;
+  for (int d = 0; d < ndim; ++d) {
+    if (shape[d] < 0 || src_pg[d] < 1 || dst_pg[d] < 1) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_repartition: bad shape or pgrid entry");
+    ns *= src_pg[d];
+    nd *= dst_pg[d];
+  }
+  if (ns != nranks || nd != nranks)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_repartition: both partitions must have exactly comm-size workers");
+  const Box mine_s = box_of(ndim, shape, src_pg, rank);
+  const Box mine_d = box_of(ndim, shape, dst_pg, rank);
+  // workspace: packed send [sum over peers] + packed recv [sum over peers]
+  std::vector<long long> scount(nranks), rcount(nranks);
+  std::vector<Box> sbox(nranks), rbox(nranks);
+  long long stot = 0, rtot = 0;
+  for (int q = 0; q < nranks; ++q) {
+    Box o;
+    scount[q] = intersect(ndim, mine_s, box_of(ndim, shape, dst_pg, q), &o) ? box_elems(ndim, o) : 0;
+    sbox[q] = o;
+    rcount[q] = intersect(ndim, box_of(ndim, shape, src_pg, q), mine_d, &o) ? box_elems(ndim, o) : 0;
+    rbox[q] = o;
+    stot += scount[q];
+    rtot += rcount[q];
+  }
+  const size_t need = align256(size_t(stot) * elem_bytes) + align256(size_t(rtot) * elem_bytes);
+  if (!workspace) {
+    *ws_bytes = need;
+    return FNO_OK;
+  }
+  if (*ws_bytes < need) return fail(FNO_ERR_WORKSPACE, "fno_repartition: workspace too small");
+  if ((stot && !src_local) || (rtot && !dst_local)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_repartition: NULL local buffer");
+  if (nranks > 1 && (!comm || !comm->nccl)) return fail(FNO_ERR_INVALID_STATE, "fno_repartition: communicator missing");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* sbuf = static_cast<char*>(workspace);
+  char* rbuf = sbuf + align256(size_t(stot) * elem_bytes);
+  long long sext[8], dext[8];
+  for (int d = 0; d < ndim; ++d) {
+    sext[d] = mine_s.hi[d] - mine_s.lo[d];
+    dext[d] = mine_d.hi[d] - mine_d.lo[d];
+  }
+  // pack (peer order ascending)
+  long long so = 0;
+  for (int q = 0; q < nranks; ++q) {
+    if (!scount[q]) continue;
+    long long lo[8], cnt[8], zero[8] = {0};
+    for (int d = 0; d < ndim; ++d) {
+      lo[d] = sbox[q].lo[d] - mine_s.lo[d];
+      cnt[d] = sbox[q].hi[d] - sbox[q].lo[d];
+    }
+    FNO_CUDA(launch_box_copy(src_local, sext, lo, sbuf + so * elem_bytes, cnt, zero, cnt, ndim, elem_bytes, st), "repartition pack");
+    so += scount[q];
+  }
+  if (nranks > 1) {
+    FNO_NCCL(ncclGroupStart(), "repartition: ncclGroupStart");
+    long long s2 = 0, r2 = 0;
+    for (int q = 0; q < nranks; ++q) {
+      if (scount[q]) FNO_NCCL(ncclSend(sbuf + s2 * elem_bytes, size_t(scount[q]) * elem_bytes, ncclUint8, q, comm->nccl, st), "repartition: ncclSend");
+      if (rcount[q]) FNO_NCCL(ncclRecv(rbuf + r2 * elem_bytes, size_t(rcount[q]) * elem_bytes, ncclUint8, q, comm->nccl, st), "repartition: ncclRecv");
+      s2 += scount[q];
+      r2 += rcount[q];
+    }
+    FNO_NCCL(ncclGroupEnd(), "repartition: ncclGroupEnd");
+  } else if (stot) {
+    FNO_CUDA(cudaMemcpyAsync(rbuf, sbuf, size_t(stot) * elem_bytes, cudaMemcpyDeviceToDevice, st), "repartition self copy");
+  }
+  // unpack
+  long long ro = 0;
+  for (int q = 0; q < nranks; ++q) {
+    if (!rcount[q]) continue;
+    long long lo[8], cnt[8], zero[8] = {0};
+    for (int d = 0; d < ndim; ++d) {
+      lo[d] = rbox[q].lo[d] - mine_d.lo[d];
+      cnt[d] = rbox[q].hi[d] - rbox[q].lo[d];
+    }
+    FNO_CUDA(launch_box_copy(rbuf + ro * elem_bytes, cnt, zero, dst_local, dext, lo, cnt, ndim, elem_bytes, st), "repartition unpack");
+    ro += rcount[q];
+  }
+  return FNO_OK;
+}

@@ -1,0 +1,151 @@
+// Shared device-side building blocks and kernel parameter blocks of libfno.
+//
+// Truncated DFTs by residue decomposition.  For an axis of length n with a set
+// of needed frequencies that maps injectively onto the residues mod L (L | n),
+//   forward:  X[k] = sum_{q<Q} w_n^{-k q} FFT_L(x[q + Q s])[k mod L]
+//   inverse:  x[r + Q s] = IFFT_L( X~[j] w_n^{+k_j r} )[s]
+// with Q = n / L.  Only the retained modes are ever formed (R_phi
+// is non-zero only at the low modes), and the FFT_L codelets (fft.cuh) keep
+// every inner twiddle a compile-time immediate; only the Q-way combine uses a
+// runtime twiddle table held in shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fft.cuh"
+
+#define FNO_MAXP 64
+
+namespace fno {
+
+// ---------------------------------------------------------------------------
+// parameter blocks (passed by value)
+// ---------------------------------------------------------------------------
+
+// Exchange buffer ordered by kz owner: chunk d = [B][Xl][Yl][C][nkz_d][mt]
+// (written by pass A, read by pass C).
+struct KzSlab {
+  int P;
+  int kz_lo[FNO_MAXP + 1];   // owner d holds retained kz [kz_lo[d], kz_lo[d+1])
+  long long off[FNO_MAXP];   // complex-element offset of chunk d
+};
+
+enum { MODE_V = 0, MODE_DZ_GELU = 1, MODE_DZ_NONE = 2 };  // pass A input
+enum { EPI_U = 0, EPI_FWD = 1, EPI_BWD = 2 };            // pass C epilogue
+
+struct PassAParams {
+  const float* in0;     // v (MODE_V) or dy
+  const float* in1;     // z_saved (MODE_DZ_GELU)
+  float2* out;          // kz-ordered slab
+  long long n_planes;   // B*C*Xl*Yl
+  int Z, T, mz, mt, Qz, Qt, NP;
+  int C, Xl, Yl;
+  KzSlab slab;
+};
+
+struct PassCParams {
+  const float2* in;     // kz-ordered slab (after exchange 2)
+  const float* v;       // EPI_FWD: v; EPI_BWD: v (for dW)
+  const float* dy;      // EPI_BWD
+  const float* zs;      // EPI_BWD: z_saved
+  const float* W;       // [C][C] (C_out, C_in)
+  const float* bias;    // nullable
+  float* out;           // u / y / dv
+  float* zsave;         // EPI_FWD, nullable
+  float* dWpart;        // EPI_BWD: [gridDim.x][C*C + C] per-CTA partial dW, db
+  long long n_cols;     // B*Xl*Yl
+  int B, C, Xl, Yl, Z, T, mz, mt, Qz, Qt;
+  int act_gelu;         // 1: sigma = GELU, 0: identity
+  float inv_n;          // 1 / (X Y Z T)
+  KzSlab slab;
+};
+
+// Pass B pencil kernels (x/y transforms on the kz-block after exchange 1).
+// Exchange buffer ordered by x/y source: chunk s = [B][Xl][Yl][C][nkz][mt].
+struct PassBParams {
+  const float2* in;
+  float2* out;
+  int B, C, X, Y, Xl, Yl, py, nkz, mt, mx, my, Q;
+  long long chunk;      // B*Xl*Yl*C*nkz*mt
+};
+
+struct MixParams {
+  const float2* vhat;   // [B][C][M]
+  const float2* R;      // [C][C][M]
+  const float2* ghat;   // bwd: [B][C][M] = F dz
+  float2* what;         // fwd: [B][C][M] mixed; bwd: [B][C][M] = R^H G^
+  float2* dR;           // bwd, nullable
+  long long M;          // 4 mx my nkz mt
+  int B, C, mt, T;
+  int accumulate;
+  float inv_n;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+
+// w[j] = exp(-2 pi i j / n), j < n, computed in double and rounded once.
+__device__ __forceinline__ void fill_twiddles(float2* w, int n, int tid, int nthreads) {
+  for (int j = tid; j < n; j += nthreads) {
+    double s, c;
+    sincospi(-2.0 * double(j) / double(n), &s, &c);
+    w[j] = make_float2(float(c), float(s));
+  }
+}
+
+// frequency (mod n) represented by residue j of an L-point transform when the
+// needed frequencies are {0..L-1-mneg} ∪ {-mneg..-1}
+__device__ __forceinline__ int kmod_of(int j, int L, int n, int mneg) {
+  return (j >= L - mneg) ? (n - L + j) : j;
+}
+
+__device__ __forceinline__ float gelu_f(float z) {
+  return 0.5f * z * (1.0f + erff(z * 0.70710678118654752440f));
+}
+__device__ __forceinline__ float gelu_prime_f(float z) {
+  return 0.5f * (1.0f + erff(z * 0.70710678118654752440f)) +
+         z * 0.39894228040143267794f * expf(-0.5f * z * z);
+}
+
+// forward truncated DFT of one pencil: acc[j] for every residue j (see header)
+template <int L, class Load>
+__device__ __forceinline__ void trunc_fwd(float2 (&acc)[L], int n, int Q, int mneg, const float2* __restrict__ twn,
+                                          Load load) {
+  for (int q = 0; q < Q; ++q) {
+    float2 x[L];
+#pragma unroll
+    for (int s = 0; s < L; ++s) x[s] = load(q + Q * s);
+    fft<L, -1>(x);
+    if (q == 0) {
+#pragma unroll
+      for (int j = 0; j < L; ++j) acc[j] = x[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        const int idx = int((long long)kmod_of(j, L, n, mneg) * q % n);
+        acc[j] = cfma(x[j], twn[idx], acc[j]);
+      }
+    }
+  }
+}
+
+// inverse truncated DFT for residue class r: y[s] = x[r + Q s]
+template <int L>
+__device__ __forceinline__ void trunc_inv(float2 (&y)[L], const float2 (&e)[L], int n, int Q, int r, int mneg,
+                                          const float2* __restrict__ twn) {
+  if (r == 0) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) y[j] = e[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const int idx = int((long long)kmod_of(j, L, n, mneg) * r % n);
+      y[j] = cmul(e[j], cconj(twn[idx]));
+    }
+  }
+  fft<L, +1>(y);
+}
+
+}  // namespace fno

@@ -1,0 +1,53 @@
+// Host-side launchers of the libfno kernels and the supported transform sizes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+// (LZ, LT) register-FFT pairs instantiated for passes A and C.  LZ covers the
+// real z-axis transform (needs mz+1 residues), LT the t-axis (needs
+// min(2mt-1, T) residues).  Chosen by the plan as the smallest supported
+// divisor of Z / T that is large enough; see fno_plan_create.
+#define FNO_AC_PAIRS(X) \
+  X(2, 4)               \
+  X(4, 5)               \
+  X(8, 8)               \
+  X(8, 16)              \
+  X(16, 15)             \
+  X(16, 16)             \
+  X(16, 30)             \
+  X(16, 32)             \
+  X(32, 32)
+
+// L values instantiated for the pass-B pencil kernels (x and y transforms,
+// need 2m residues).
+#define FNO_B_SIZES(X) X(2) X(4) X(5) X(6) X(8) X(16) X(30) X(32)
+
+namespace fno {
+
+size_t pass_a_smem(int Z, int T, int mz, int NP);
+cudaError_t launch_pass_a(const PassAParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
+
+size_t pass_c_smem(int C, int Z, int T, int mz, int mt, int LZ, int mode);
+cudaError_t launch_pass_c(const PassCParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
+
+// pass B: y forward (slab -> H), x forward (H -> V^), x inverse (W^ -> H'),
+// y inverse (H' -> slab)
+cudaError_t launch_b_yfwd(const PassBParams& p, int L, cudaStream_t st);
+cudaError_t launch_b_xfwd(const PassBParams& p, int L, cudaStream_t st);
+cudaError_t launch_b_xinv(const PassBParams& p, int L, cudaStream_t st);
+cudaError_t launch_b_yinv(const PassBParams& p, int L, cudaStream_t st);
+
+cudaError_t launch_mix_fwd(const MixParams& p, cudaStream_t st);
+cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st);
+
+// deterministic fixed-order sum of nparts rows of `len` floats; columns
+// [0, split) go to out0, the rest to out1 (nullable); out = sum or out += sum
+cudaError_t launch_rowsum(const float* parts, int nparts, int len, int split, float* out0, float* out1, int accumulate,
+                          cudaStream_t st);
+
+bool ac_pair_supported(int LZ, int LT);
+bool b_size_supported(int L);
+
+}  // namespace fno

@@ -1,0 +1,319 @@
+// Pass B: the second index set I_2 = {y, x} of the distributed FFT on the
+// rank's block of retained kz planes ("then taking an FFT over the last
+// n/2 dimensions"; "2D FFT along the x and y dimensions"), the per-mode
+// channel mixing with R_phi on the owner, and the adjoint chain
+// back (F_dist^T).  SURVEY §8 rows a3 (fwd x,y), a4 (mixing), a5
+// (inverse x,y), a11 (dR).
+//
+// Layouts:  exchange buffer by x/y source / destination:
+//             [s][B][Xl][Yl][C][nkz][mt]  (s = ix*py + iy, chunk = B Xl Yl C nkz mt)
+//           H  (after the y transform)   [B][nkz][C][X][2my][mt]
+//           V^, W^, G^ (mode cube)       [B][C][2mx][2my][nkz][mt]
+//           R, dR                        [C][C][2mx][2my][nkz][mt]
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace fno {
+
+static constexpr int BT = 128;  // threads per CTA of the pencil kernels
+
+// y forward: slab (x/y-source ordered) -> H.  pencil = (b, kzl, c, x, kt)
+template <int L>
+__global__ void __launch_bounds__(BT) b_yfwd_kernel(PassBParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);               // Y
+  long long* ypart = reinterpret_cast<long long*>(tw + p.Y);      // Y
+  const int cm = p.C * p.nkz * p.mt;
+  for (int y = threadIdx.x; y < p.Y; y += blockDim.x) ypart[y] = (long long)(y / p.Yl) * p.chunk + (long long)(y % p.Yl) * cm;
+  fill_twiddles(tw, p.Y, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
+  const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= total) return;
+  const int kt = int(pid % p.mt);
+  long long r = pid / p.mt;
+  const int x = int(r % p.X);
+  r /= p.X;
+  const int c = int(r % p.C);
+  r /= p.C;
+  const int kzl = int(r % p.nkz);
+  const int b = int(r / p.nkz);
+  const int sx = x / p.Xl, xl = x - sx * p.Xl;
+  const long long xpart = (long long)sx * p.py * p.chunk + ((long long)b * p.Xl + xl) * p.Yl * cm +
+                          (long long)(c * p.nkz + kzl) * p.mt + kt;
+  const float2* __restrict__ in = p.in;
+  float2 acc[L];
+  trunc_fwd<L>(acc, p.Y, p.Q, p.my, tw, [&](int y) { return __ldg(in + xpart + ypart[y]); });
+  float2* o = p.out + (((long long)(b * p.nkz + kzl) * p.C + c) * p.X + x) * (2 * p.my) * p.mt + kt;
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    if (j < p.my) o[(long long)j * p.mt] = acc[j];
+    else if (j >= L - p.my) o[(long long)(j - L + 2 * p.my) * p.mt] = acc[j];
+  }
+}
+
+// x forward: H -> V^.  pencil = (b, kzl, c, jy, kt)
+template <int L>
+__global__ void __launch_bounds__(BT) b_xfwd_kernel(PassBParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  fill_twiddles(tw, p.X, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int my2 = 2 * p.my;
+  const long long total = (long long)p.B * p.nkz * p.C * my2 * p.mt;
+  const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= total) return;
+  const int kt = int(pid % p.mt);
+  long long r = pid / p.mt;
+  const int jy = int(r % my2);
+  r /= my2;
+  const int c = int(r % p.C);
+  r /= p.C;
+  const int kzl = int(r % p.nkz);
+  const int b = int(r / p.nkz);
+  const float2* __restrict__ in = p.in + ((long long)(b * p.nkz + kzl) * p.C + c) * p.X * my2 * p.mt + jy * p.mt + kt;
+  const long long xs = (long long)my2 * p.mt;
+  float2 acc[L];
+  trunc_fwd<L>(acc, p.X, p.Q, p.mx, tw, [&](int x) { return __ldg(in + x * xs); });
+  const int mx2 = 2 * p.mx;
+  float2* o = p.out + ((((long long)b * p.C + c) * mx2) * my2 + jy) * p.nkz * p.mt + (long long)kzl * p.mt + kt;
+  const long long js = (long long)my2 * p.nkz * p.mt;
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    if (j < p.mx) o[j * js] = acc[j];
+    else if (j >= L - p.mx) o[(j - L + mx2) * js] = acc[j];
+  }
+}
+
+// x inverse: W^ -> H'.  pencil = (b, kzl, o, jy, kt); loops over residue classes
+template <int L>
+__global__ void __launch_bounds__(BT) b_xinv_kernel(PassBParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  fill_twiddles(tw, p.X, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int my2 = 2 * p.my, mx2 = 2 * p.mx;
+  const long long total = (long long)p.B * p.nkz * p.C * my2 * p.mt;
+  const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= total) return;
+  const int kt = int(pid % p.mt);
+  long long r = pid / p.mt;
+  const int jy = int(r % my2);
+  r /= my2;
+  const int oc = int(r % p.C);
+  r /= p.C;
+  const int kzl = int(r % p.nkz);
+  const int b = int(r / p.nkz);
+  const float2* __restrict__ in = p.in + ((((long long)b * p.C + oc) * mx2) * my2 + jy) * p.nkz * p.mt + (long long)kzl * p.mt + kt;
+  const long long js = (long long)my2 * p.nkz * p.mt;
+  float2 e[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    if (j < p.mx) e[j] = __ldg(in + j * js);
+    else if (j >= L - p.mx) e[j] = __ldg(in + (j - L + mx2) * js);
+    else e[j] = make_float2(0.f, 0.f);
+  }
+  float2* o = p.out + ((long long)(b * p.nkz + kzl) * p.C + oc) * p.X * my2 * p.mt + jy * p.mt + kt;
+  const long long xs = (long long)my2 * p.mt;
+  for (int rc = 0; rc < p.Q; ++rc) {
+    float2 y[L];
+    trunc_inv<L>(y, e, p.X, p.Q, rc, p.mx, tw);
+#pragma unroll
+    for (int s = 0; s < L; ++s) o[(rc + p.Q * s) * xs] = y[s];
+  }
+}
+
+// y inverse: H' -> slab (x/y-destination ordered).  pencil = (b, kzl, o, x, kt)
+template <int L>
+__global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  long long* ypart = reinterpret_cast<long long*>(tw + p.Y);
+  const int cm = p.C * p.nkz * p.mt;
+  for (int y = threadIdx.x; y < p.Y; y += blockDim.x) ypart[y] = (long long)(y / p.Yl) * p.chunk + (long long)(y % p.Yl) * cm;
+  fill_twiddles(tw, p.Y, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int my2 = 2 * p.my;
+  const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
+  const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= total) return;
+  const int kt = int(pid % p.mt);
+  long long r = pid / p.mt;
+  const int x = int(r % p.X);
+  r /= p.X;
+  const int oc = int(r % p.C);
+  r /= p.C;
+  const int kzl = int(r % p.nkz);
+  const int b = int(r / p.nkz);
+  const float2* __restrict__ in = p.in + (((long long)(b * p.nkz + kzl) * p.C + oc) * p.X + x) * my2 * p.mt + kt;
+  float2 e[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    if (j < p.my) e[j] = __ldg(in + (long long)j * p.mt);
+    else if (j >= L - p.my) e[j] = __ldg(in + (long long)(j - L + my2) * p.mt);
+    else e[j] = make_float2(0.f, 0.f);
+  }
+  const int sx = x / p.Xl, xl = x - sx * p.Xl;
+  float2* o = p.out + (long long)sx * p.py * p.chunk + ((long long)b * p.Xl + xl) * p.Yl * cm +
+              (long long)(oc * p.nkz + kzl) * p.mt + kt;
+  for (int rc = 0; rc < p.Q; ++rc) {
+    float2 y[L];
+    trunc_inv<L>(y, e, p.Y, p.Q, rc, p.my, tw);
+#pragma unroll
+    for (int s = 0; s < L; ++s) o[ypart[rc + p.Q * s]] = y[s];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-mode channel mixing (R_phi . F v on owned modes)
+// thread per retained mode m; complex fp32 accumulation
+// ---------------------------------------------------------------------------
+template <int CMAX>
+__global__ void __launch_bounds__(128) mix_fwd_kernel(MixParams p) {
+  const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= p.M) return;
+  const int C = p.C;
+  for (int b = 0; b < p.B; ++b) {
+    float2 vh[CMAX];
+#pragma unroll
+    for (int i = 0; i < CMAX; ++i)
+      if (i < C) vh[i] = __ldg(p.vhat + ((long long)b * C + i) * p.M + m);
+    for (int o = 0; o < C; ++o) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < CMAX; ++i)
+        if (i < C) acc = cfma(vh[i], __ldcs(p.R + ((long long)i * C + o) * p.M + m), acc);
+      p.what[((long long)b * C + o) * p.M + m] = acc;
+    }
+  }
+}
+
+// backward mixing: W'^[b,i,m] = sum_o G^[b,o,m] conj(R[i,o,m]);
+// dR[i,o,m] (+)= (c(kt)/N) sum_b conj(V^[b,i,m]) G^[b,o,m]
+template <int CMAX>
+__global__ void __launch_bounds__(128) mix_bwd_kernel(MixParams p) {
+  const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= p.M) return;
+  const int C = p.C;
+  const int kt = int(m % p.mt);
+  const float cw = (kt == 0 || ((p.T & 1) == 0 && 2 * kt == p.T)) ? 1.0f : 2.0f;
+  const float scale = cw * p.inv_n;
+  for (int b = 0; b < p.B; ++b) {
+    float2 g[CMAX];
+#pragma unroll
+    for (int o = 0; o < CMAX; ++o)
+      if (o < C) g[o] = __ldg(p.ghat + ((long long)b * C + o) * p.M + m);
+    for (int i = 0; i < C; ++i) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < CMAX; ++o)
+        if (o < C) acc = cfma_conj_a(__ldg(p.R + ((long long)i * C + o) * p.M + m), g[o], acc);
+      p.what[((long long)b * C + i) * p.M + m] = acc;
+    }
+  }
+  if (p.dR != nullptr) {
+    for (int i = 0; i < C; ++i) {
+      for (int o = 0; o < C; ++o) {
+        float2 acc = make_float2(0.f, 0.f);
+        for (int b = 0; b < p.B; ++b)
+          acc = cfma_conj_a(__ldg(p.vhat + ((long long)b * C + i) * p.M + m), __ldg(p.ghat + ((long long)b * C + o) * p.M + m), acc);
+        float2* d = p.dR + ((long long)i * C + o) * p.M + m;
+        float2 val = cscale(acc, scale);
+        if (p.accumulate) val = cadd(*d, val);
+        *d = val;
+      }
+    }
+  }
+}
+
+// deterministic fixed-order (ascending row) column sums; columns [0, split)
+// go to out0, [split, len) to out1 (nullable)
+__global__ void rowsum_kernel(const float* __restrict__ parts, int nparts, int len, int split, float* out0, float* out1,
+                              int accumulate) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= len) return;
+  float s = 0.f;
+  for (int p = 0; p < nparts; ++p) s += parts[(long long)p * len + l];
+  float* o = (l < split) ? out0 + l : (out1 ? out1 + (l - split) : nullptr);
+  if (o) *o = accumulate ? *o + s : s;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <class K>
+static cudaError_t launch_pencils(K k, const PassBParams& p, long long total, size_t smem, cudaStream_t st) {
+  if (total <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const long long grid = (total + BT - 1) / BT;
+  k<<<unsigned(grid), BT, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_b_yfwd(const PassBParams& p, int L, cudaStream_t st) {
+  const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
+  const size_t smem = size_t(p.Y) * (sizeof(float2) + sizeof(long long));
+#define FNO_CASE(l) if (L == l) return launch_pencils(b_yfwd_kernel<l>, p, total, smem, st);
+  FNO_B_SIZES(FNO_CASE)
+#undef FNO_CASE
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_b_xfwd(const PassBParams& p, int L, cudaStream_t st) {
+  const long long total = (long long)p.B * p.nkz * p.C * 2 * p.my * p.mt;
+  const size_t smem = size_t(p.X) * sizeof(float2);
+#define FNO_CASE(l) if (L == l) return launch_pencils(b_xfwd_kernel<l>, p, total, smem, st);
+  FNO_B_SIZES(FNO_CASE)
+#undef FNO_CASE
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_b_xinv(const PassBParams& p, int L, cudaStream_t st) {
+  const long long total = (long long)p.B * p.nkz * p.C * 2 * p.my * p.mt;
+  const size_t smem = size_t(p.X) * sizeof(float2);
+#define FNO_CASE(l) if (L == l) return launch_pencils(b_xinv_kernel<l>, p, total, smem, st);
+  FNO_B_SIZES(FNO_CASE)
+#undef FNO_CASE
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_b_yinv(const PassBParams& p, int L, cudaStream_t st) {
+  const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
+  const size_t smem = size_t(p.Y) * (sizeof(float2) + sizeof(long long));
+#define FNO_CASE(l) if (L == l) return launch_pencils(b_yinv_kernel<l>, p, total, smem, st);
+  FNO_B_SIZES(FNO_CASE)
+#undef FNO_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <class K>
+static cudaError_t launch_mix(K k, const MixParams& p, cudaStream_t st) {
+  if (p.M <= 0) return cudaSuccess;
+  k<<<unsigned((p.M + 127) / 128), 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_mix_fwd(const MixParams& p, cudaStream_t st) {
+  if (p.C <= 8) return launch_mix(mix_fwd_kernel<8>, p, st);
+  if (p.C <= 32) return launch_mix(mix_fwd_kernel<32>, p, st);
+  if (p.C <= 64) return launch_mix(mix_fwd_kernel<64>, p, st);
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st) {
+  if (p.C <= 8) return launch_mix(mix_bwd_kernel<8>, p, st);
+  if (p.C <= 32) return launch_mix(mix_bwd_kernel<32>, p, st);
+  if (p.C <= 64) return launch_mix(mix_bwd_kernel<64>, p, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rowsum(const float* parts, int nparts, int len, int split, float* out0, float* out1, int accumulate,
+                          cudaStream_t st) {
+  rowsum_kernel<<<(len + 127) / 128, 128, 0, st>>>(parts, nparts, len, split, out0, out1, accumulate);
+  return cudaGetLastError();
+}
+
+bool b_size_supported(int L) {
+#define FNO_CASE(l) if (L == l) return true;
+  FNO_B_SIZES(FNO_CASE)
+#undef FNO_CASE
+  return false;
+}
+
+}  // namespace fno

@@ -1,0 +1,187 @@
+"""GPU parity: libfno's sm_100a path vs the fp64 oracle on the same seeded fp32
+inputs.  Bar (north star, BASELINE.json): relative L2 <= 1e-5 for the fp32 path
+on u, y, z, V^, dv, dR, dW, db."""
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import spectral as sp
+from tests._instances import rel_l2, worked_example
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2204_01205_b200 import build
+    build.build()
+
+
+def _problem(grid, C, modes, B=1, seed=0, shape="ns"):
+    v = synth.field((B, C) + tuple(grid), modes, seed, shape)
+    R = synth.spectral_weights(C, C, modes, seed + 1)
+    W, b = synth.channel_weights(C, seed + 2)
+    dy = synth.cotangent(v.shape, seed + 3)
+    return v, R, W, b, dy
+
+
+# (grid, C, modes, B): c1 itself plus every instantiated (LZ, LT) pair, shrunk in x/y
+CASES = [
+    ((16, 16, 16, 8), 4, (4, 4, 4, 4), 1),        # c1 (BASELINE configs[0])
+    ((32, 16, 64, 32), 20, (8, 8, 8, 8), 1),      # c2 shape class, x/y shrunk
+    ((32, 32, 64, 30), 6, (12, 12, 12, 12), 1),   # c3 shape class (T=30, 2mz does not divide Z)
+    ((32, 32, 128, 32), 4, (12, 12, 12, 12), 1),  # c4 shape class
+    ((32, 32, 256, 32), 2, (16, 16, 16, 16), 1),  # c5 shape class
+    ((12, 10, 12, 10), 3, (3, 2, 3, 3), 2),       # odd sizes, C % 4 != 0, batch 2
+    ((8, 8, 8, 8), 5, (4, 4, 4, 5), 1),           # full pass incl. Nyquist kt = T/2
+    ((16, 8, 16, 8), 2, (2, 2, 4, 4), 3),         # (LZ, LT) = (8, 8), ragged batch of 3
+]
+
+
+def _ids(c):
+    return "x".join(map(str, c[0])) + f"_C{c[1]}_m{'-'.join(map(str, c[2]))}_B{c[3]}"
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
+def test_layer_forward_matches_oracle(case):
+    from tests import _gpu as G
+    grid, C, modes, B = case
+    v, R, W, b, _ = _problem(grid, C, modes, B, seed=101)
+    plan = G.make_plan(grid, C, modes, B)
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    y_ref, z_ref = sp.layer_fwd(G.f32(v), G.f32(R), G.f32(W), G.f32(b), modes)
+    vh_ref = sp.forward_modes(G.f32(v), modes)
+    assert rel_l2(G.np64(vh), vh_ref) < TOL
+    assert rel_l2(G.np64(z), z_ref) < TOL
+    assert rel_l2(G.np64(y), y_ref) < TOL
+
+
+@pytest.mark.parametrize("case", CASES[:3] + CASES[5:], ids=_ids)
+def test_spectral_conv_forward_and_adjoint(case):
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    grid, C, modes, B = case
+    v, R, W, b, g = _problem(grid, C, modes, B, seed=202)
+    plan = G.make_plan(grid, C, modes, B)
+    u, vh = G.spectral_fwd(plan, v, R)
+    u_ref = sp.spectral_conv(G.f32(v), G.f32(R), modes)
+    assert rel_l2(G.np64(u), u_ref) < TOL
+    gt = G.t32(g)
+    dv = torch.empty_like(gt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    fno.spectral_conv_bwd(plan, gt, G.tc64(R), vh, dv, dR)
+    torch.cuda.synchronize()
+    dv_ref = sp.spectral_conv_adjoint(G.f32(g), G.f32(R), modes)
+    assert rel_l2(G.np64(dv), dv_ref) < TOL
+    _, dR_ref, _, _ = sp.layer_bwd(G.f32(v), G.f32(g), G.f32(R), 0 * G.f32(W), None, modes, act="none")
+    assert rel_l2(G.np64(dR), dR_ref) < TOL
+    # adjoint identity on the GPU results (pin P9, fp32)
+    lhs = float(np.sum(G.np64(u) * G.f32(g)))
+    rhs = float(np.sum(G.f32(v) * G.np64(dv)))
+    assert abs(lhs - rhs) / (np.linalg.norm(G.np64(u)) * np.linalg.norm(g)) < 1e-6
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
+@pytest.mark.parametrize("act", ["gelu", "none"])
+def test_layer_backward_matches_oracle(case, act):
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    grid, C, modes, B = case
+    if act == "none" and case not in (CASES[0], CASES[5]):
+        pytest.skip("act=none covered on two shapes")
+    v, R, W, b, dy = _problem(grid, C, modes, B, seed=303)
+    plan = G.make_plan(grid, C, modes, B, act=act)
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    dyt = G.t32(dy)
+    dv = torch.empty_like(dyt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.empty((C, C), dtype=torch.float32, device="cuda")
+    db = torch.empty((C,), dtype=torch.float32, device="cuda")
+    fno.layer_bwd(plan, G.t32(v), z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db)
+    torch.cuda.synchronize()
+    dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes, act=act)
+    assert rel_l2(G.np64(dv), dv_r) < TOL
+    assert rel_l2(G.np64(dR), dR_r) < TOL
+    assert rel_l2(G.np64(dW), dW_r) < TOL
+    assert rel_l2(G.np64(db), db_r) < TOL
+    # accumulate = 1 adds into dR, dW, db
+    fno.layer_bwd(plan, G.t32(v), z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_l2(G.np64(dR), 2 * dR_r) < TOL
+    assert rel_l2(G.np64(dW), 2 * dW_r) < TOL
+    assert rel_l2(G.np64(db), 2 * db_r) < TOL
+
+
+def test_golden_worked_example_on_gpu():
+    from tests import _gpu as G
+    ex = worked_example()
+    plan = G.make_plan(ex["grid"], 2, ex["modes"])
+    u, _ = G.spectral_fwd(plan, ex["v"], ex["R"])
+    y, _, _ = G.layer_fwd(plan, ex["v"], ex["R"], ex["W"], ex["b"])
+    u = G.np64(u)[0]
+    y = G.np64(y)[0]
+    e = ex["expected"]
+    assert abs(u.sum() - e["sum_u"]) < 1e-4
+    assert abs((u ** 2).sum() - e["sum_u2"]) / e["sum_u2"] < 1e-5
+    assert abs(u[0, 0, 0, 0, 0] - e["u[0,0,0,0,0]"]) < 1e-5
+    assert abs(u[1, 1, 2, 3, 1] - e["u[1,1,2,3,1]"]) < 1e-5
+    assert abs(y.sum() - e["sum_y"]) / abs(e["sum_y"]) < 1e-5
+    assert abs(y[1, 3, 0, 2, 2] - e["y[1,3,0,2,2]"]) < 1e-5
+
+
+def test_identity_weights_full_pass_is_identity_on_gpu():
+    """Pin P6 on the GPU: m = n/2, mt = T/2 + 1, R = I per mode -> S v = v."""
+    from tests import _gpu as G
+    grid, C, modes = (8, 8, 8, 8), 3, (4, 4, 4, 5)
+    v, _, _, _, _ = _problem(grid, C, modes, 1, seed=404)
+    R = np.zeros((C, C, 8, 8, 8, 5), dtype=np.complex64)
+    for i in range(C):
+        R[i, i] = 1.0
+    plan = G.make_plan(grid, C, modes)
+    u, _ = G.spectral_fwd(plan, v, R)
+    assert rel_l2(G.np64(u), G.f32(v)) < TOL
+
+
+def test_zero_weights_give_gelu_of_zero():
+    from tests import _gpu as G
+    grid, C, modes = (16, 16, 16, 8), 4, (4, 4, 4, 4)
+    v, R, W, b, _ = _problem(grid, C, modes, 1, seed=505)
+    plan = G.make_plan(grid, C, modes)
+    y, _, _ = G.layer_fwd(plan, v, 0 * R, 0 * W, 0 * b)
+    assert float(np.max(np.abs(G.np64(y)))) == 0.0
+
+
+@pytest.mark.slow
+def test_full_size_c2_sampled_outputs():
+    """BASELINE configs[1] at full size (64^3 x 32, C=20, m=8), the launch
+    configuration bench.py times; the oracle evaluates 512 sampled points."""
+    import torch
+    from tests import _gpu as G
+    cfg = synth.CONFIGS[2]
+    grid, C, modes = cfg["grid"], cfg["width"], cfg["modes"]
+    pr = synth.problem(2, with_dy=False)
+    plan = G.make_plan(grid, C, modes)
+    y, z, vh = G.layer_fwd(plan, pr["v"], pr["R"], pr["W"], pr["b"])
+    v64 = G.f32(pr["v"])
+    vh_ref = sp.forward_modes(v64, modes)
+    assert rel_l2(G.np64(vh), vh_ref) < TOL
+    what = sp.mix(vh_ref, G.f32(pr["R"]))
+    rng = np.random.default_rng(7)
+    pts = np.stack([rng.integers(0, n, size=512) for n in grid], -1)
+    u_s = sp.inverse_modes_at(what, grid, pts)[0]                      # [C, P]
+    vs = v64[0][:, pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]          # [C, P]
+    z_ref = G.f32(pr["W"]) @ vs + G.f32(pr["b"])[:, None] + u_s
+    zg = G.np64(z)[0][:, pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+    yg = G.np64(y)[0][:, pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+    assert rel_l2(zg, z_ref) < TOL
+    assert rel_l2(yg, sp.gelu(z_ref)) < TOL
+    del y, z, vh
+    torch.cuda.empty_cache()
