@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the 4D FNO spectral-layer hot path (arXiv 2204.01205).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+A step is one training pass of the whole hot path over
+one synthetic batch: the forward of `layers` DFNO blocks in training mode
+(storing z and V^), then their backward (dv, dR, dW, db), on the BASELINE.json
+configs[1] shape (4D Navier-Stokes-shaped: 64x64x64x32 per GPU, width 20,
+modes 8, 4 Fourier layers, batch 1).  Multi-GPU runs are weak-scaled exactly
+like the paper's App. A spatial study: the per-GPU box stays
+64x64x64x32 and the global grid grows over an x/y process grid
+(1,1) (2,1) (2,2) (4,2), with the pencil all-to-all over NCCL/NVLink.
+
+metric: grid-points x channels x layers processed (fwd+bwd) per second, whole
+job; value = B * X*Y*Z*T (global) * C * layers / step time (max over ranks).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "4D FNO layer grid-pts·ch/s fwd+bwd at 1/2/4/8 B200; % HBM/NVLink roofline"
+PGRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+CONFIG_INDEX = 2            # BASELINE.json configs[1] (c2)
+REF_WIDTH = 4               # oracle sample: channels per reference step
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML polling thread)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+        0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, indices, period=0.005):
+        self.indices, self.period = indices, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.handles = [pynvml.nvmlDeviceGetHandleByUUID(i) if isinstance(i, str)
+                            else pynvml.nvmlDeviceGetHandleByIndex(i) for i in indices]
+            self.max_mhz = max(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM) for h in self.handles)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            for h in self.handles:
+                try:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit and name != "gpu_idle":
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def nvml_index(cuda_index):
+    """NVML handle key of a CUDA device (UUID; falls back to the index)."""
+    try:
+        import torch
+        u = str(torch.cuda.get_device_properties(cuda_index).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return cuda_index
+
+
+# ---------------------------------------------------------------------------
+# roofline bookkeeping (algorithmic bytes per launch)
+# ---------------------------------------------------------------------------
+def stage_bytes(prob, plan_info):
+    """Algorithmic HBM bytes per launch of each kernel stage (fp32 / complex64)."""
+    B, C = prob["B"], prob["C"]
+    Xl, Yl, Z, T = prob["local"]
+    X, Y = prob["grid"][0], prob["grid"][1]
+    mx, my, mz, mt = prob["modes"]
+    nkz = plan_info["nkz"]
+    P = prob["P"]
+    n = B * C * Xl * Yl * Z * T                       # local field elements
+    slab = 8 * B * C * Xl * Yl * 2 * mz * mt          # bytes of this rank's slab (send side)
+    slab_kz = 8 * P * B * C * Xl * Yl * nkz * mt      # bytes of the kz-block slab (after exchange)
+    M = 4 * mx * my * nkz * mt
+    H = 8 * B * nkz * C * X * 2 * my * mt
+    mode = 8 * B * C * M
+    Rb = 8 * C * C * M
+    return {
+        "fwd.pass_a": 4 * n + slab,
+        "fwd.b_y_fwd": slab_kz + H,
+        "fwd.b_x_fwd": H + mode,
+        "fwd.mix": Rb + 2 * mode,
+        "fwd.b_x_inv": mode + H,
+        "fwd.b_y_inv": H + slab_kz,
+        "fwd.pass_c": slab + 4 * n + 4 * n + 4 * n,         # slab, v, y, z_save
+        "bwd.pass_a": 8 * n + slab,                          # dy, z -> slab
+        "bwd.b_y_fwd": slab_kz + H,
+        "bwd.b_x_fwd": H + mode,
+        "bwd.mix": 2 * Rb + 3 * mode,                        # R, dR, V^, G^, W'^
+        "bwd.b_x_inv": mode + H,
+        "bwd.b_y_inv": H + slab_kz,
+        "bwd.pass_c": slab + 12 * n + 4 * n,                 # slab, dy, z, v, dv
+        "fwd.exchange_1": slab * (P - 1) / P, "fwd.exchange_2": slab * (P - 1) / P,
+        "bwd.exchange_1": slab * (P - 1) / P, "bwd.exchange_2": slab * (P - 1) / P,
+    }
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_01205_b200 as fno
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synth.CONFIGS[CONFIG_INDEX]
+    lx, ly, Z, T = cfg["grid"]
+    C, modes, L = cfg["width"], cfg["modes"], args.layers or cfg["layers"]
+    B = args.batch
+    px, py = PGRIDS[world]
+    grid = (lx * px, ly * py, Z, T)
+    comm = fno.Comm.from_process_group() if world > 1 else None
+    plan = fno.Plan(fno.Problem(grid=grid, width=C, modes=modes, batch=B, pgrid=(px, py)), comm, device=dev)
+    kz_lo, kz_hi = plan.owned_modes()
+    local = plan.local_shape()
+    # inputs (synthetic, seeded; field on device, weights from the numpy recipe)
+    seed = synth.seed_for(CONFIG_INDEX, 0, salt=rank)
+    v0 = synth.field_torch(local, modes, seed, cfg["shape"], device=dev)
+    dy = torch.randn(local, generator=torch.Generator(device=dev).manual_seed(seed + 3), device=dev)
+    Rs, Ws, bs = [], [], []
+    for layer in range(L):
+        s = synth.seed_for(CONFIG_INDEX, layer)
+        R = synth.spectral_weights(C, C, modes, s + 1, kz_range=(kz_lo, kz_hi))
+        W, b = synth.channel_weights(C, s + 2)
+        Rs.append(torch.from_numpy(R).to(dev))
+        Ws.append(torch.from_numpy(W).to(dev))
+        bs.append(torch.from_numpy(b).to(dev))
+    acts = [v0] + [torch.empty_like(v0) for _ in range(L)]
+    zs = [torch.empty_like(v0) for _ in range(L)]
+    vhs = [torch.empty(plan.vhat_shape(), dtype=torch.complex64, device=dev) for _ in range(L)]
+    dR = [torch.empty(plan.weight_shape(), dtype=torch.complex64, device=dev) for _ in range(L)]
+    dW = torch.empty((L, C, C), device=dev)
+    db = torch.empty((L, C), device=dev)
+    g = [dy, torch.empty_like(v0), torch.empty_like(v0)]
+
+    def step():
+        for l in range(L):
+            fno.layer_fwd(plan, acts[l], Rs[l], Ws[l], bs[l], acts[l + 1], zs[l], vhs[l])
+        cur = 0                      # g[0] = upstream dy; dv ping-pongs between g[1], g[2]
+        for l in reversed(range(L)):
+            nxt = 1 if cur != 1 else 2
+            fno.layer_bwd(plan, acts[l], zs[l], vhs[l], g[cur], Rs[l], Ws[l], g[nxt], dR[l], dW[l], db[l])
+            cur = nxt
+
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region (device clock, CUDA events on the launching stream) ----
+    plan.profile_enable(True)
+    plan.profile_read()
+    n0 = fno.kernel_launches()
+    sampler = ClockSampler([nvml_index(local_rank)])
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        end.synchronize()
+        barrier()
+    launches = fno.kernel_launches() - n0
+    prof = plan.profile_read()
+    plan.profile_enable(False)
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    units = B * grid[0] * grid[1] * grid[2] * grid[3] * C * L
+    value = units / (ms_step / 1e3)
+
+    # ---- end to end: pinned host inputs -> device, step, result -> host -------
+    h_v = torch.empty(local, dtype=torch.float32, pin_memory=True)
+    h_dy = torch.empty(local, dtype=torch.float32, pin_memory=True)
+    h_v.copy_(v0.cpu())
+    h_dy.copy_(dy.cpu())
+    h_out = torch.empty((L, C * C + C), dtype=torch.float32, pin_memory=True)
+    res = torch.empty((L, C * C + C), device=dev)
+
+    def e2e_step():
+        acts[0].copy_(h_v, non_blocking=True)
+        g[0].copy_(h_dy, non_blocking=True)
+        step()
+        res[:, :C * C].copy_(dW.view(L, C * C))
+        res[:, C * C:].copy_(db)
+        h_out.copy_(res, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    e1.synchronize()
+    t2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t2.item()) / args.steps
+    e2e_value = units / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel -----------------------------------
+    info = dict(nkz=kz_hi - kz_lo)
+    prob = dict(B=B, C=C, local=local[2:], grid=grid, modes=modes, P=world)
+    sb = stage_bytes(prob, info)
+    kern = {k: v for k, v in prof.items() if "exchange" not in k and k in sb}
+    dom = max(kern, key=lambda k: kern[k][0]) if kern else None
+    peak, peak_kind = load_peaks()
+    roof = None
+    if dom:
+        tot_ms, cnt = kern[dom]
+        avg_s = tot_ms / cnt / 1e3
+        ach = sb[dom] / avg_s / 1e9
+        traffic = load_traffic().get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": traffic, "algorithmic_bytes": int(sb[dom]), "avg_launch_us": round(avg_s * 1e6, 2),
+                "share_of_step": round(tot_ms / max(sum(v[0] for v in prof.values()), 1e-9), 4)}
+    stages = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps,
+                  "GBps": (round(sb[k] / (v[0] / v[1] / 1e3) / 1e9, 1) if k in sb else None)}
+              for k, v in sorted(prof.items())}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ---
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(args, v0.detach().cpu().numpy(), dy.detach().cpu().numpy(), modes, repeats=1)
+
+    clocks = sampler.summary()
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "grid-pts·ch/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded NS-shaped fields, random-init weights)",
+        "config": {"workload": "c2: 4D Navier-Stokes-shaped DFNO training step (fwd+bwd), 64x64x64x32 per GPU, "
+                               "width 20, modes 8, 4 Fourier layers, batch 1 (BASELINE.json configs[1])",
+                   "global_grid": list(grid), "pgrid": [px, py], "batch": B, "width": C, "modes": list(modes),
+                   "layers": L, "parallelism": f"x/y domain decomposition {px}x{py}",
+                   "l2": "inputs larger than L2 (671 MB field per layer per GPU)"},
+        "e2e": {"value": round(e2e_value, 1), "unit": "grid-pts·ch/s", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": int(h_v.numel() * 4 + h_dy.numel() * 4),
+                "d2h_bytes_per_step": int(h_out.numel() * 4)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "stages": stages,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+    plan.destroy()
+    if comm:
+        comm.destroy()
+
+
+def oracle_sample(args, v, dy, modes, repeats=1):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    one DFNO block forward + backward on the full per-GPU grid, REF_WIDTH of
+    the 20 channels.  Returns the cpu_baseline object (grid-pts·ch/s)."""
+    import numpy as np
+
+    import synth
+    from oracle import spectral as sp
+    C = REF_WIDTH
+    vs = np.asarray(v[:, :C], dtype=np.float64)
+    dys = np.asarray(dy[:, :C], dtype=np.float64)
+    s = synth.seed_for(CONFIG_INDEX, 0)
+    R = synth.spectral_weights(C, C, modes, s + 1).astype(np.complex128)
+    W, b = synth.channel_weights(C, s + 2)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        sp.layer_fwd(vs, R, W.astype(np.float64), b.astype(np.float64), modes)
+        sp.layer_bwd(vs, dys, R, W.astype(np.float64), b.astype(np.float64), modes)
+        times.append(time.perf_counter() - t0)
+    t = min(times)
+    units = vs.size          # grid points x channels of one layer, fwd+bwd
+    cores = len(os.sched_getaffinity(0))
+    return {"value": round(units / t, 1), "unit": "grid-pts·ch/s", "cores": cores, "kind": "oracle",
+            "sample": f"one DFNO block fwd+bwd (oracle.spectral.layer_fwd + layer_bwd, fp64 numpy, naive DFT "
+                      f"matrices) on the full per-GPU grid {list(v.shape[2:])}, width {C} of 20, batch 1; "
+                      f"{t:.2f} s wall",
+            "seconds": round(t, 3)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle on the host cores (rank 0 only)
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+
+    import synth
+    cfg = synth.CONFIGS[CONFIG_INDEX]
+    lx, ly, Z, T = cfg["grid"]
+    modes = cfg["modes"]
+    shape = (1, REF_WIDTH, lx, ly, Z, T)
+    s = synth.seed_for(CONFIG_INDEX, 0)
+    v = synth.field(shape, modes, s, cfg["shape"], n_waves=4)
+    dy = synth.cotangent(shape, s + 3)
+    for _ in range(args.warmup):
+        oracle_sample(args, v, dy, modes)
+    t0 = time.perf_counter()
+    res = [oracle_sample(args, v, dy, modes) for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    units = float(np.prod(shape))
+    value = units * args.steps / wall
+    cpu = dict(res[0])
+    cpu["value"] = round(value, 1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "grid-pts·ch/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * wall / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded NS-shaped fields, random-init weights)",
+        "config": {"workload": "c2 per-GPU grid 64x64x64x32, modes 8; oracle sample: one DFNO block fwd+bwd at "
+                               f"width {REF_WIDTH} of 20 per step (bounded CPU sample)",
+                   "grid": [lx, ly, Z, T], "width": REF_WIDTH, "modes": list(modes), "batch": 1},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(value, 1), "unit": "grid-pts·ch/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torch.distributed.run",
+              file=sys.stderr)
+        if world == 1:
+            args.gpus = 1
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world not in PGRIDS:
+        raise SystemExit(f"unsupported world size {world} (1, 2, 4, 8)")
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -156,6 +156,22 @@ fno_status fno_repartition(fno_comm_t comm, int ndim, const int64_t* global_shap
                            const int32_t* dst_pgrid, size_t elem_bytes, const void* src_local, void* dst_local,
                            void* workspace, size_t* ws_bytes, void* stream);
 
+/* ---- instrumentation ------------------------------------------------------ */
+/* When enabled, every stage of every call on this plan (pass A, exchange 1,
+ * the pass-B kernels, mixing, exchange 2, pass C, the dW reduction) is
+ * bracketed by CUDA events recorded on the call's stream (CUDA
+ * events per stage).  fno_plan_profile_read waits for the recorded events and
+ * returns, per stage i < fno_profile_stage_count(), the summed milliseconds and
+ * the number of timed launches since the last read; then it resets.  nstages
+ * must be >= fno_profile_stage_count(). */
+fno_status fno_plan_profile_enable(fno_plan_t plan, int enable);
+fno_status fno_plan_profile_read(fno_plan_t plan, double* ms, int64_t* count, int nstages);
+int fno_profile_stage_count(void);
+const char* fno_profile_stage_name(int stage);
+/* Number of kernels this process has launched through libfno (NCCL's own
+ * kernels are not counted). */
+unsigned long long fno_kernel_launches(void);
+
 const char* fno_status_string(fno_status s);
 const char* fno_last_error(void);
 int fno_abi_version(void);

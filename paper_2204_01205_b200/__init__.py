@@ -76,6 +76,14 @@ def lib() -> ctypes.CDLL:
             f = getattr(L, name)
             f.argtypes = args
             f.restype = ctypes.c_int
+        L.fno_plan_profile_enable.argtypes = [vp, i32]
+        L.fno_plan_profile_enable.restype = ctypes.c_int
+        L.fno_plan_profile_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64), i32]
+        L.fno_plan_profile_read.restype = ctypes.c_int
+        L.fno_profile_stage_count.restype = ctypes.c_int
+        L.fno_profile_stage_name.argtypes = [ctypes.c_int]
+        L.fno_profile_stage_name.restype = ctypes.c_char_p
+        L.fno_kernel_launches.restype = ctypes.c_ulonglong
         L.fno_status_string.argtypes = [ctypes.c_int]
         L.fno_status_string.restype = ctypes.c_char_p
         L.fno_last_error.argtypes = []
@@ -229,6 +237,17 @@ class Plan:
         s = self.weight_shape()
         return (self.problem.batch,) + s[1:]
 
+    def profile_enable(self, on: bool = True):
+        _check(lib().fno_plan_profile_enable(self.handle, int(bool(on))), "fno_plan_profile_enable")
+
+    def profile_read(self):
+        """{stage name: (total ms, launches)} since the last read (waits for the events)."""
+        n = lib().fno_profile_stage_count()
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(lib().fno_plan_profile_read(self.handle, ms, cnt, n), "fno_plan_profile_read")
+        return {lib().fno_profile_stage_name(i).decode(): (ms[i], cnt[i]) for i in range(n) if cnt[i]}
+
     def destroy(self):
         if self.handle:
             lib().fno_plan_destroy(self.handle)
@@ -239,6 +258,11 @@ class Plan:
             self.destroy()
         except Exception:
             pass
+
+
+def kernel_launches() -> int:
+    """Kernels launched through libfno by this process so far."""
+    return int(lib().fno_kernel_launches())
 
 
 def _contig(*ts):
@@ -297,4 +321,4 @@ def repartition(comm: Optional[Comm], global_shape, src_pgrid, dst_pgrid, src_lo
 
 
 __all__ = ["Problem", "Comm", "Plan", "FnoError", "lib", "spectral_conv_fwd", "spectral_conv_bwd", "layer_fwd",
-           "layer_bwd", "repartition", "LIB_PATH"]
+           "layer_bwd", "repartition", "kernel_launches", "LIB_PATH"]

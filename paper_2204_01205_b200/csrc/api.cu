@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -60,6 +61,20 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+enum Stage { ST_PASS_A, ST_EX1, ST_B_YF, ST_B_XF, ST_MIX, ST_B_XI, ST_B_YI, ST_EX2, ST_PASS_C, ST_DW, ST_N };
+static const char* kStageNames[2 * ST_N] = {
+    "fwd.pass_a", "fwd.exchange_1", "fwd.b_y_fwd", "fwd.b_x_fwd", "fwd.mix", "fwd.b_x_inv", "fwd.b_y_inv", "fwd.exchange_2", "fwd.pass_c", "fwd.unused",
+    "bwd.pass_a", "bwd.exchange_1", "bwd.b_y_fwd", "bwd.b_x_fwd", "bwd.mix", "bwd.b_x_inv", "bwd.b_y_inv", "bwd.exchange_2", "bwd.pass_c", "bwd.dw_reduce"};
+
+static std::atomic<unsigned long long> g_launches{0};
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> recs;  // (stage, index of start event)
+};
+
 struct fno_comm_s {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0;
@@ -87,7 +102,51 @@ struct fno_plan_s {
   size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, total;
   size_t n_slab_xy, n_slab_kz, n_h, n_mode;
   int max_grid_c = 0;
+  int dir = 0;  // 0 forward call, 1 backward call (profiling labels)
+  Prof prof;
+  ~fno_plan_s() {
+    for (cudaEvent_t e : prof.ev) cudaEventDestroy(e);
+  }
 };
+
+namespace {
+// records CUDA events around one stage on the launching stream when profiling
+struct StageScope {
+  fno_plan_t p;
+  int stage;
+  cudaStream_t st;
+  size_t i0 = 0;
+  bool on;
+  size_t next() {
+    if (p->prof.used == p->prof.ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      p->prof.ev.push_back(e);
+    }
+    return p->prof.used++;
+  }
+  StageScope(fno_plan_t p_, int s, cudaStream_t st_) : p(p_), stage(s), st(st_), on(p_->prof.on) {
+    if (on) {
+      i0 = next();
+      next();
+      cudaEventRecord(p->prof.ev[i0], st);
+    }
+  }
+  ~StageScope() {
+    if (on) {
+      cudaEventRecord(p->prof.ev[i0 + 1], st);
+      p->prof.recs.emplace_back(stage + p->dir * ST_N, i0);
+    }
+  }
+};
+}  // namespace
+
+#define FNO_LAUNCH(p, stage, call, what) \
+  do {                                   \
+    StageScope _sc((p), (stage), st);    \
+    FNO_CUDA(call, what);                \
+    g_launches++;                        \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // status / version
@@ -327,6 +386,31 @@ extern "C" fno_status fno_plan_owned_modes(fno_plan_t p, int32_t* kz_lo, int32_t
   return FNO_OK;
 }
 
+extern "C" fno_status fno_plan_profile_enable(fno_plan_t p, int enable) {
+  if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_profile_enable: NULL plan");
+  p->prof.on = enable != 0;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_profile_read(fno_plan_t p, double* ms, int64_t* count, int nstages) {
+  if (!p || !ms || !count || nstages < 2 * ST_N) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_profile_read: bad arguments");
+  for (int i = 0; i < nstages; ++i) { ms[i] = 0.0; count[i] = 0; }
+  for (auto& r : p->prof.recs) {
+    float t = 0.f;
+    FNO_CUDA(cudaEventSynchronize(p->prof.ev[r.second + 1]), "fno_plan_profile_read");
+    FNO_CUDA(cudaEventElapsedTime(&t, p->prof.ev[r.second], p->prof.ev[r.second + 1]), "fno_plan_profile_read");
+    ms[r.first] += t;
+    count[r.first] += 1;
+  }
+  p->prof.recs.clear();
+  p->prof.used = 0;
+  return FNO_OK;
+}
+
+extern "C" int fno_profile_stage_count(void) { return 2 * ST_N; }
+extern "C" const char* fno_profile_stage_name(int i) { return (i >= 0 && i < 2 * ST_N) ? kStageNames[i] : ""; }
+extern "C" unsigned long long fno_kernel_launches(void) { return g_launches.load(); }
+
 extern "C" fno_status fno_plan_vhat_elems(fno_plan_t p, size_t* elems) {
   if (!p || !elems) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_vhat_elems: NULL argument");
   *elems = p->n_mode;
@@ -372,6 +456,7 @@ fno_status exchange_fwd(fno_plan_t p, cudaStream_t st) {
   const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;  // complex per kz plane
   float2* send = wsp<float2>(p, p->o_slab_xy);
   float2* recv = wsp<float2>(p, p->o_slab_kz);
+  StageScope sc(p, ST_EX1, st);
   FNO_NCCL(ncclGroupStart(), "exchange 1: ncclGroupStart");
   for (int d = 0; d < p->P; ++d) {
     const size_t ns = per * (p->kz_lo[d + 1] - p->kz_lo[d]);
@@ -390,6 +475,7 @@ fno_status exchange_bwd(fno_plan_t p, cudaStream_t st) {
   const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;
   float2* send = wsp<float2>(p, p->o_slab_kz);
   float2* recv = wsp<float2>(p, p->o_slab_xy);
+  StageScope sc(p, ST_EX2, st);
   FNO_NCCL(ncclGroupStart(), "exchange 2: ncclGroupStart");
   for (int d = 0; d < p->P; ++d) {
     const size_t ns = per * p->nkz;
@@ -409,7 +495,7 @@ fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode
   a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->NP;
   a.C = p->C; a.Xl = int(p->Xl); a.Yl = int(p->Yl);
   a.slab = make_kzslab(p);
-  FNO_CUDA(launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a, p->smem_a, st), "pass A");
+  FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a, p->smem_a, st), "pass A");
   return FNO_OK;
 }
 
@@ -418,8 +504,8 @@ fno_status run_b_fwd(fno_plan_t p, float2* vhat_out, cudaStream_t st) {
   if (p->nkz == 0) return FNO_OK;
   float2* slab = wsp<float2>(p, p->o_slab_kz);
   float2* H = wsp<float2>(p, p->o_h);
-  FNO_CUDA(launch_b_yfwd(make_b(p, slab, H, p->Qy), p->LY, st), "pass B y-forward");
-  FNO_CUDA(launch_b_xfwd(make_b(p, H, vhat_out, p->Qx), p->LX, st), "pass B x-forward");
+  FNO_LAUNCH(p, ST_B_YF, launch_b_yfwd(make_b(p, slab, H, p->Qy), p->LY, st), "pass B y-forward");
+  FNO_LAUNCH(p, ST_B_XF, launch_b_xfwd(make_b(p, H, vhat_out, p->Qx), p->LX, st), "pass B x-forward");
   return FNO_OK;
 }
 
@@ -428,8 +514,8 @@ fno_status run_b_inv(fno_plan_t p, const float2* what, cudaStream_t st) {
   if (p->nkz == 0) return FNO_OK;
   float2* slab = wsp<float2>(p, p->o_slab_kz);
   float2* H = wsp<float2>(p, p->o_h);
-  FNO_CUDA(launch_b_xinv(make_b(p, what, H, p->Qx), p->LX, st), "pass B x-inverse");
-  FNO_CUDA(launch_b_yinv(make_b(p, H, slab, p->Qy), p->LY, st), "pass B y-inverse");
+  FNO_LAUNCH(p, ST_B_XI, launch_b_xinv(make_b(p, what, H, p->Qx), p->LX, st), "pass B x-inverse");
+  FNO_LAUNCH(p, ST_B_YI, launch_b_yinv(make_b(p, H, slab, p->Qy), p->LY, st), "pass B y-inverse");
   return FNO_OK;
 }
 
@@ -474,7 +560,7 @@ fno_status spectral_fwd_to_slab(fno_plan_t p, const float* v, const float2* R, f
   if (p->nkz > 0) {
     MixParams m = make_mix(p);
     m.vhat = vhat; m.R = R; m.what = wsp<float2>(p, p->o_what);
-    FNO_CUDA(launch_mix_fwd(m, st), "mixing (forward)");
+    FNO_LAUNCH(p, ST_MIX, launch_mix_fwd(m, st), "mixing (forward)");
   }
   FNO_TRY(run_b_inv(p, wsp<float2>(p, p->o_what), st));
   FNO_TRY(exchange_bwd(p, st));
@@ -492,7 +578,7 @@ fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1
     MixParams m = make_mix(p);
     m.vhat = vhat_saved; m.R = R; m.ghat = ghat; m.what = wsp<float2>(p, p->o_what);
     m.dR = dR; m.accumulate = accumulate;
-    FNO_CUDA(launch_mix_bwd(m, st), "mixing (backward)");
+    FNO_LAUNCH(p, ST_MIX, launch_mix_bwd(m, st), "mixing (backward)");
   }
   FNO_TRY(run_b_inv(p, wsp<float2>(p, p->o_what), st));
   FNO_TRY(exchange_bwd(p, st));
@@ -504,19 +590,21 @@ fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1
 extern "C" fno_status fno_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
                                             void* stream) {
   FNO_TRY(check_ready(p, "fno_spectral_conv_fwd"));
+  p->dir = 0;
   if (!v || !u || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_fwd: NULL data pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
   FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
   PassCParams c = make_c(p);
   c.out = u;
-  FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (u)");
+  FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (u)");
   return FNO_OK;
 }
 
 extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
                                             float* dv, void* dR, int accumulate, void* stream) {
   FNO_TRY(check_ready(p, "fno_spectral_conv_bwd"));
+  p->dir = 1;
   if (!g || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: NULL g or R");
   if (dR && !vhat_saved && p->nkz > 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: dR requires vhat_saved");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -525,7 +613,7 @@ extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const 
   if (dv) {
     PassCParams c = make_c(p);
     c.out = dv;
-    FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (adjoint u)");
+    FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (adjoint u)");
   }
   return FNO_OK;
 }
@@ -533,13 +621,14 @@ extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const 
 extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
                                     float* z_save, void* vhat_save, void* stream) {
   FNO_TRY(check_ready(p, "fno_layer_fwd"));
+  p->dir = 0;
   if (!v || !W || !y || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_fwd: NULL data pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
   FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
   PassCParams c = make_c(p);
   c.v = v; c.W = W; c.bias = b; c.out = y; c.zsave = z_save;
-  FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
+  FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
   return FNO_OK;
 }
 
@@ -547,6 +636,7 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
                                     const float* dy, const void* R, const float* W, float* dv, void* dR, float* dW,
                                     float* db, int accumulate, void* stream) {
   FNO_TRY(check_ready(p, "fno_layer_bwd"));
+  p->dir = 1;
   if (!v || !dy || !W || !dv || !dW || (!R && p->nkz > 0) || (p->act_gelu && !z_saved))
     return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_bwd: NULL data pointer (v, dy, W, dv, dW, R and z_saved for GELU are required)");
   if (dR && !vhat_saved && p->nkz > 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_bwd: dR requires vhat_saved");
@@ -557,16 +647,16 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
   PassCParams c = make_c(p);
   c.v = v; c.dy = dy; c.zs = z_saved; c.W = W; c.out = dv;
   c.dWpart = wsp<float>(p, p->o_dwpart);
-  FNO_CUDA(launch_pass_c(c, p->LZ, p->LT, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
+  FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
   const int len = p->C * p->C + p->C;
   if (p->P == 1) {
-    FNO_CUDA(launch_rowsum(c.dWpart, p->grid_c_bwd, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, p->grid_c_bwd, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
   } else {
     float* loc = wsp<float>(p, p->o_dwloc);
     float* all = wsp<float>(p, p->o_dwall);
-    FNO_CUDA(launch_rowsum(c.dWpart, p->grid_c_bwd, len, len, loc, nullptr, 0, st), "dW/db local reduction");
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, p->grid_c_bwd, len, len, loc, nullptr, 0, st), "dW/db local reduction");
     FNO_NCCL(ncclAllGather(loc, all, size_t(len), ncclFloat, p->comm->nccl, st), "dW/db all-gather");
-    FNO_CUDA(launch_rowsum(all, p->P, len, p->C * p->C, dW, db, accumulate, st), "dW/db rank-ordered sum");
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(all, p->P, len, p->C * p->C, dW, db, accumulate, st), "dW/db rank-ordered sum");
   }
   return FNO_OK;
 }
@@ -669,6 +759,7 @@ extern "C" fno_status fno_repartition(fno_comm_t comm, int ndim, const int64_t* 
       cnt[d] = sbox[q].hi[d] - sbox[q].lo[d];
     }
     FNO_CUDA(launch_box_copy(src_local, sext, lo, sbuf + so * elem_bytes, cnt, zero, cnt, ndim, elem_bytes, st), "repartition pack");
+    g_launches++;
     so += scount[q];
   }
   if (nranks > 1) {
@@ -694,6 +785,7 @@ extern "C" fno_status fno_repartition(fno_comm_t comm, int ndim, const int64_t* 
       cnt[d] = rbox[q].hi[d] - rbox[q].lo[d];
     }
     FNO_CUDA(launch_box_copy(rbuf + ro * elem_bytes, cnt, zero, dst_local, dext, lo, cnt, ndim, elem_bytes, st), "repartition unpack");
+    g_launches++;
     ro += rcount[q];
   }
   return FNO_OK;

@@ -68,10 +68,45 @@ def field(shape, modes, seed: int, kind: str = "ns", n_waves: int = 8, noise: fl
                 amp = 1.0 / (1.0 + sum(k * k for k in ks))
                 ph = rng.uniform(0, 2 * np.pi, size=4)
                 f = [np.cos(2 * np.pi * k * a / n + p) for k, a, n, p in zip(ks, ax, (X, Y, Z, T), ph)]
-                acc += amp * np.einsum("x,y,z,t->xyzt", *f)
+                acc += amp * (f[0][:, None, None, None] * f[1][None, :, None, None] * f[2][None, None, :, None] *
+                              f[3][None, None, None, :])
             if kind == "co2":
                 acc *= (0.25 + ax[3] / max(T - 1, 1))[None, None, None, :]
             out[b, c] += acc.astype(np.float32)
+    return out
+
+
+def field_torch(shape, modes, seed: int, kind: str = "ns", n_waves: int = 8, noise: float = 0.1, device="cuda"):
+    """Same recipe as `field`, drawn on the device with torch (for bench-sized
+    fields; a different random stream than the numpy version)."""
+    import math
+
+    import torch
+    B, C, X, Y, Z, T = (int(s) for s in shape)
+    mx, my, mz, mt = (int(m) for m in modes)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    out = noise * torch.randn((B, C, X, Y, Z, T), generator=g, device=device, dtype=torch.float32)
+    rng = np.random.default_rng(seed)
+    ax = [torch.arange(n, device=device, dtype=torch.float32) for n in (X, Y, Z, T)]
+    ramp = (0.25 + ax[3] / max(T - 1, 1)) if kind == "co2" else None
+    for b in range(B):
+        for c in range(C):
+            acc = torch.zeros((X, Y, Z, T), device=device, dtype=torch.float32)
+            for w in range(n_waves):
+                inside = (w % 2 == 0)
+                ks = [int(_wave_numbers(rng, n, m, 1, inside)[0]) for n, m in zip((X, Y, Z, T), (mx, my, mz, mt))]
+                if kind == "co2":
+                    ks[0] = ks[0] // 4 if abs(ks[0]) >= 4 else ks[0]
+                    ks[1] = ks[1] // 4 if abs(ks[1]) >= 4 else ks[1]
+                amp = 1.0 / (1.0 + sum(k * k for k in ks))
+                ph = rng.uniform(0, 2 * np.pi, size=4)
+                f = [torch.cos(2 * math.pi * k * a / n + float(p)) for k, a, n, p in zip(ks, ax, (X, Y, Z, T), ph)]
+                acc += amp * (f[0][:, None, None, None] * f[1][None, :, None, None] * f[2][None, None, :, None] *
+                              f[3][None, None, None, :])
+            if ramp is not None:
+                acc *= ramp
+            out[b, c] += acc
     return out
 
 
