@@ -91,10 +91,11 @@ struct fno_plan_s {
   int nkz = 0;             // own block
   int LZ, LT, LX, LY;
   int Qz, Qt, Qx, Qy;
-  int NP;                  // planes per pass-A batch
   int num_sms = 148;
-  int grid_a = 1, grid_c = 1, grid_c_bwd = 1;
-  size_t smem_a = 0, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
+  int grid_c = 1, grid_c_bwd = 1;
+  size_t smem_a[3] = {0, 0, 0}, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
+  int np_a[3] = {1, 1, 1}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
+  int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -242,6 +243,7 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   if (pb->grid[0] % pb->pgrid[0] || pb->grid[1] % pb->pgrid[1])
     return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_create: X % px and Y % py must be 0 (balanced uneven boxes are not supported yet)");
   if (2 * pb->modes[2] > 32767) return fail(FNO_ERR_PLAN, "fno_plan_create: too many z modes");
+  if (pb->grid[3] > 512 || pb->grid[2] > 4096) return fail(FNO_ERR_PLAN, "fno_plan_create: T > 512 or Z > 4096 not supported");
 
   auto* p = new fno_plan_s();
   p->pb = *pb;
@@ -300,24 +302,25 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
     cudaGetLastError();
   }
 
-  // pass A batching: ~256 pencils and <= 48 KB of staged planes per batch
-  const long long ZT = p->Z * p->T;
-  p->NP = int(std::max<long long>(1, std::min<long long>(256 / p->T, (48 * 1024) / (ZT * 4))));
-  p->smem_a = pass_a_smem(int(p->Z), int(p->T), p->mz, p->NP);
-  p->smem_c_u = pass_c_smem(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_U);
-  p->smem_c_fwd = pass_c_smem(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD);
-  p->smem_c_bwd = pass_c_smem(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD);
+  // pass A batching (planes per TMA batch) per input mode
+  for (int m = 0; m < 3; ++m) pass_a_config(int(p->Z), int(p->T), p->mz, m, &p->np_a[m], &p->smem_a[m], &p->tma_a);
+  pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_U, &p->tch[0], &p->vw[0], &p->smem_c_u);
+  pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
+  pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
   const size_t smem_max = 227 * 1024;
-  if (p->smem_a > smem_max || p->smem_c_bwd > smem_max) {
+  if (p->smem_a[MODE_DZ_GELU] > smem_max || p->smem_c_bwd > smem_max) {
     char buf[200];
-    std::snprintf(buf, sizeof buf, "fno_plan_create: shared memory per CTA too large (pass A %zu, pass C %zu bytes)", p->smem_a, p->smem_c_bwd);
+    std::snprintf(buf, sizeof buf, "fno_plan_create: shared memory per CTA too large (pass A %zu, pass C %zu bytes)",
+                  p->smem_a[MODE_DZ_GELU], p->smem_c_bwd);
     delete p;
     return fail(FNO_ERR_PLAN, buf);
   }
   const long long n_planes = (long long)p->B * p->C * p->Xl * p->Yl;
-  const long long n_batches = (n_planes + p->NP - 1) / p->NP;
-  const int per_sm_a = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (p->smem_a + 1024))));
-  p->grid_a = int(std::max<long long>(1, std::min<long long>(n_batches, (long long)p->num_sms * per_sm_a)));
+  for (int m = 0; m < 3; ++m) {
+    const long long n_batches = (n_planes + p->np_a[m] - 1) / p->np_a[m];
+    const int per_sm_a = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (p->smem_a[m] + 1024))));
+    p->grid_a_m[m] = int(std::max<long long>(1, std::min<long long>(n_batches, (long long)p->num_sms * per_sm_a)));
+  }
   const long long n_cols = (long long)p->B * p->Xl * p->Yl;
   auto grid_for = [&](size_t smem) {
     const int per_sm = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (smem + 1024))));
@@ -492,10 +495,11 @@ fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode
   a.in0 = in0; a.in1 = in1;
   a.out = wsp<float2>(p, p->o_slab_xy);
   a.n_planes = (long long)p->B * p->C * p->Xl * p->Yl;
-  a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->NP;
+  a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->np_a[mode];
   a.C = p->C; a.Xl = int(p->Xl); a.Yl = int(p->Yl);
+  a.use_tma = p->tma_a;
   a.slab = make_kzslab(p);
-  FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a, p->smem_a, st), "pass A");
+  FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a_m[mode], p->smem_a[mode], st), "pass A");
   return FNO_OK;
 }
 
@@ -526,8 +530,10 @@ MixParams make_mix(fno_plan_t p) {
   return m;
 }
 
-PassCParams make_c(fno_plan_t p) {
+PassCParams make_c(fno_plan_t p, int mode) {
   PassCParams c{};
+  c.TCH = p->tch[mode];
+  c.VW = p->vw[mode];
   c.in = wsp<float2>(p, p->o_slab_xy);
   c.n_cols = (long long)p->B * p->Xl * p->Yl;
   c.B = p->B; c.C = p->C; c.Xl = int(p->Xl); c.Yl = int(p->Yl); c.Z = int(p->Z); c.T = int(p->T);
@@ -595,7 +601,7 @@ extern "C" fno_status fno_spectral_conv_fwd(fno_plan_t p, const float* v, const 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
   FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
-  PassCParams c = make_c(p);
+  PassCParams c = make_c(p, EPI_U);
   c.out = u;
   FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (u)");
   return FNO_OK;
@@ -611,7 +617,7 @@ extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const 
   FNO_TRY(spectral_bwd_to_slab(p, g, nullptr, MODE_V, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
                                static_cast<float2*>(dR), accumulate, st));
   if (dv) {
-    PassCParams c = make_c(p);
+    PassCParams c = make_c(p, EPI_U);
     c.out = dv;
     FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (adjoint u)");
   }
@@ -626,7 +632,7 @@ extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
   FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
-  PassCParams c = make_c(p);
+  PassCParams c = make_c(p, EPI_FWD);
   c.v = v; c.W = W; c.bias = b; c.out = y; c.zsave = z_save;
   FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
   return FNO_OK;
@@ -644,7 +650,7 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
   const int mode = p->act_gelu ? MODE_DZ_GELU : MODE_DZ_NONE;
   FNO_TRY(spectral_bwd_to_slab(p, dy, z_saved, mode, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
                                static_cast<float2*>(dR), accumulate, st));
-  PassCParams c = make_c(p);
+  PassCParams c = make_c(p, EPI_BWD);
   c.v = v; c.dy = dy; c.zs = z_saved; c.W = W; c.out = dv;
   c.dWpart = wsp<float>(p, p->o_dwpart);
   FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");

@@ -41,6 +41,7 @@ struct PassAParams {
   long long n_planes;   // B*C*Xl*Yl
   int Z, T, mz, mt, Qz, Qt, NP;
   int C, Xl, Yl;
+  int use_tma;          // 1: TMA bulk copies of plane batches (Z*T % 4 == 0)
   KzSlab slab;
 };
 
@@ -56,6 +57,7 @@ struct PassCParams {
   float* dWpart;        // EPI_BWD: [gridDim.x][C*C + C] per-CTA partial dW, db
   long long n_cols;     // B*Xl*Yl
   int B, C, Xl, Yl, Z, T, mz, mt, Qz, Qt;
+  int TCH, VW;          // t-chunk of a tile, cp.async vector width (floats)
   int act_gelu;         // 1: sigma = GELU, 0: identity
   float inv_n;          // 1 / (X Y Z T)
   KzSlab slab;
@@ -86,6 +88,55 @@ struct MixParams {
 // helpers
 // ---------------------------------------------------------------------------
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// Ampere-style cp.async (LDGSTS): any 4/8/16-byte aligned element
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// TMA bulk copy (cp.async.bulk, UBLKCP) global -> shared, completion counted in
+// bytes on an mbarrier (16-byte aligned addresses, size multiple of 16)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+
 // w[j] = exp(-2 pi i j / n), j < n, computed in double and rounded once.
 __device__ __forceinline__ void fill_twiddles(float2* w, int n, int tid, int nthreads) {
   for (int j = tid; j < n; j += nthreads) {
@@ -109,41 +160,59 @@ __device__ __forceinline__ float gelu_prime_f(float z) {
          z * 0.39894228040143267794f * expf(-0.5f * z * z);
 }
 
-// forward truncated DFT of one pencil: acc[j] for every residue j (see header)
+// Q-way combine twiddles of a truncated DFT, one row per residue class:
+//   tab[q*L + j] = exp(sign * 2 pi i * kmod_j * q / n),  q < Q, j < L
+// (n = Q*L entries).  Computed once per CTA in double, rounded once.
+__device__ __forceinline__ void fill_combine_table(float2* tab, int L, int Q, int n, int mneg, int sign, int tid,
+                                                   int nthreads) {
+  for (int e = tid; e < L * Q; e += nthreads) {
+    const int q = e / L, j = e - q * L;
+    const long long k = kmod_of(j, L, n, mneg);
+    const long long r = (k * q) % n;
+    double sn, cs;
+    sincospi(2.0 * double(sign) * double(r) / double(n), &sn, &cs);
+    tab[e] = make_float2(float(cs), float(sn));
+  }
+}
+
+// forward truncated DFT of one pencil: acc[j] for every residue j (see header).
+// ctab: combine table with sign -1 (fill_combine_table(..., -1, ...)).
+// Only residues j < jpos or j >= L - jneg are combined (the others are never
+// stored by the callers).
 template <int L, class Load>
-__device__ __forceinline__ void trunc_fwd(float2 (&acc)[L], int n, int Q, int mneg, const float2* __restrict__ twn,
-                                          Load load) {
-  for (int q = 0; q < Q; ++q) {
+__device__ __forceinline__ void trunc_fwd(float2 (&acc)[L], int Q, const float2* __restrict__ ctab, Load load,
+                                          int jpos = L, int jneg = 0) {
+  {
+    float2 x[L];
+#pragma unroll
+    for (int s = 0; s < L; ++s) x[s] = load(Q * s);
+    fft<L, -1>(x);
+#pragma unroll
+    for (int j = 0; j < L; ++j) acc[j] = x[j];
+  }
+  for (int q = 1; q < Q; ++q) {
     float2 x[L];
 #pragma unroll
     for (int s = 0; s < L; ++s) x[s] = load(q + Q * s);
     fft<L, -1>(x);
-    if (q == 0) {
+    const float2* tw = ctab + q * L;
 #pragma unroll
-      for (int j = 0; j < L; ++j) acc[j] = x[j];
-    } else {
-#pragma unroll
-      for (int j = 0; j < L; ++j) {
-        const int idx = int((long long)kmod_of(j, L, n, mneg) * q % n);
-        acc[j] = cfma(x[j], twn[idx], acc[j]);
-      }
-    }
+    for (int j = 0; j < L; ++j)
+      if (j < jpos || j >= L - jneg) acc[j] = cfma(x[j], tw[j], acc[j]);
   }
 }
 
-// inverse truncated DFT for residue class r: y[s] = x[r + Q s]
+// inverse truncated DFT for residue class r: y[s] = x[r + Q s].
+// ctab: combine table with sign +1.
 template <int L>
-__device__ __forceinline__ void trunc_inv(float2 (&y)[L], const float2 (&e)[L], int n, int Q, int r, int mneg,
-                                          const float2* __restrict__ twn) {
+__device__ __forceinline__ void trunc_inv(float2 (&y)[L], const float2 (&e)[L], int r, const float2* __restrict__ ctab) {
   if (r == 0) {
 #pragma unroll
     for (int j = 0; j < L; ++j) y[j] = e[j];
   } else {
+    const float2* tw = ctab + r * L;
 #pragma unroll
-    for (int j = 0; j < L; ++j) {
-      const int idx = int((long long)kmod_of(j, L, n, mneg) * r % n);
-      y[j] = cmul(e[j], cconj(twn[idx]));
-    }
+    for (int j = 0; j < L; ++j) y[j] = cmul(e[j], tw[j]);
   }
   fft<L, +1>(y);
 }

@@ -26,10 +26,13 @@
 
 namespace fno {
 
-size_t pass_a_smem(int Z, int T, int mz, int NP);
+// planes per batch NP, dynamic shared memory and TMA eligibility for a pass-A mode
+void pass_a_config(int Z, int T, int mz, int mode, int* NP, size_t* smem, int* use_tma);
 cudaError_t launch_pass_a(const PassAParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
 
-size_t pass_c_smem(int C, int Z, int T, int mz, int mt, int LZ, int mode);
+// chooses the t-chunk TCH (largest that fits shared memory), the cp.async
+// vector width VW and the dynamic shared memory size for a pass-C mode
+void pass_c_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* TCH, int* VW, size_t* smem);
 cudaError_t launch_pass_c(const PassCParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
 
 // pass B: y forward (slab -> H), x forward (H -> V^), x inverse (W^ -> H'),

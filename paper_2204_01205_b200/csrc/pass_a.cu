@@ -11,78 +11,145 @@
 // This is the real FFT along t of P:144 ("first taking an FFT along time")
 // evaluated in the cheaper z-first order (same result by separability).
 // Output: kz-owner-ordered slab [d][B][Xl][Yl][C][nkz_d][mt] (complex).
+//
+// Streaming: a persistent CTA processes batches of NP consecutive planes (one
+// contiguous run of HBM).  Each batch is fetched by one TMA bulk copy
+// (cp.async.bulk, completion on an mbarrier) into one of two stage buffers; the
+// copy of batch k+2 is issued as soon as phase 1 of batch k has drained its
+// buffer, so HBM stays busy while the CTA transforms.
 #include "kernels.cuh"
 #include "launch.h"
 
 namespace fno {
 
+static constexpr int AT = 256;
+
+struct ALayout {
+  size_t stage[2], bb, twz, twt, dmap, bar, total;
+  int NA;
+};
+
+__host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mode) {
+  ALayout L{};
+  L.NA = (mode == MODE_DZ_GELU) ? 2 : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 127) & ~size_t(127); return o; };
+  const size_t sb = size_t(L.NA) * NP * Z * T * sizeof(float);
+  L.stage[0] = take(sb);
+  L.stage[1] = take(sb);
+  L.bb = take(size_t(NP) * (mz + 1) * (T + 1) * sizeof(float2));
+  L.twz = take(size_t(Z) * sizeof(float2));
+  L.twt = take(size_t(T) * sizeof(float2));
+  L.dmap = take(size_t(2 * mz) * sizeof(short2));
+  L.bar = take(2 * sizeof(uint64_t));
+  L.total = off;
+  return L;
+}
+
 template <int LZ, int LT, int MODE>
-__global__ void __launch_bounds__(256) pass_a_kernel(PassAParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
   const int ZT = Z * T;
   const int NP = p.NP;
   const int nk = mz + 1;        // kz' = 0..mz
   const int TP = T + 1;         // padded row of B
-  float* stage = reinterpret_cast<float*>(smem_raw);                       // NP*Z*T
-  float2* Bb = reinterpret_cast<float2*>(stage + ((NP * ZT + 3) & ~3));    // NP*nk*TP
-  float2* twZ = Bb + NP * nk * TP;                                         // Z
-  float2* twT = twZ + Z;                                                   // T
-  short2* dmap = reinterpret_cast<short2*>(twT + T);                       // 2mz: (owner d, local kz)
-
+  const ALayout L = a_layout(Z, T, mz, NP, MODE);
+  constexpr int NA = (MODE == MODE_DZ_GELU) ? 2 : 1;
+  float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
+  float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
+  float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
+  short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
   const int tid = threadIdx.x, nt = blockDim.x;
-  fill_twiddles(twZ, Z, tid, nt);
-  fill_twiddles(twT, T, tid, nt);
+  const long long n_batches = (p.n_planes + NP - 1) / NP;
+  if ((long long)blockIdx.x >= n_batches) return;
+
+  fill_combine_table(twZ, LZ, p.Qz, Z, 0, -1, tid, nt);
+  fill_combine_table(twT, LT, p.Qt, T, mt - 1, -1, tid, nt);
   for (int j = tid; j < 2 * mz; j += nt) {
     int d = 0;
     while (j >= p.slab.kz_lo[d + 1]) ++d;
     dmap[j] = make_short2(short(d), short(j - p.slab.kz_lo[d]));
   }
+  const bool tma = p.use_tma != 0;
+  if (tid == 0 && tma) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
 
-  const long long n_batches = (p.n_planes + NP - 1) / NP;
-  for (long long batch = blockIdx.x; batch < n_batches; batch += gridDim.x) {
-    const long long plane0 = batch * NP;
+  // fetch batch index kb into stage buffer sb
+  auto issue = [&](long long kb, int sb) {
+    const long long plane0 = kb * NP;
     const long long left = p.n_planes - plane0;
     const int np = left < NP ? int(left) : NP;
-    __syncthreads();  // previous batch fully consumed; tables visible
-    // ---- stage np contiguous planes -------------------------------------
-    {
-      const long long base = plane0 * ZT;
-      const int nel = np * ZT;
-      if (MODE == MODE_V || MODE == MODE_DZ_NONE) {
-        const float* src = p.in0 + base;
-        if ((nel & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-          const float4* s4 = reinterpret_cast<const float4*>(src);
-          float4* d4 = reinterpret_cast<float4*>(stage);
-          for (int i = tid; i < nel / 4; i += nt) d4[i] = __ldcs(s4 + i);
-        } else {
-          for (int i = tid; i < nel; i += nt) stage[i] = src[i];
-        }
-      } else {  // dz = dy * gelu'(z_saved)
-        const float* dy = p.in0 + base;
-        const float* zs = p.in1 + base;
-        for (int i = tid; i < nel; i += nt) stage[i] = dy[i] * gelu_prime_f(zs[i]);
+    float* dst = reinterpret_cast<float*>(smem_raw + L.stage[sb]);
+    const long long base = plane0 * ZT;
+    const unsigned bytes = unsigned(np) * ZT * sizeof(float);
+    if (tma) {
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar[sb], bytes * NA);
+        tma_load_1d(dst, p.in0 + base, bytes, &bar[sb]);
+        if (NA == 2) tma_load_1d(dst + NP * ZT, p.in1 + base, bytes, &bar[sb]);
       }
+    } else {
+      for (int i = tid; i < np * ZT; i += nt) {
+        cp_async4(dst + i, p.in0 + base + i);
+        if (NA == 2) cp_async4(dst + NP * ZT + i, p.in1 + base + i);
+      }
+      cp_commit();
     }
-    __syncthreads();
+  };
+
+  long long kb = blockIdx.x;
+  issue(kb, 0);
+  if (kb + gridDim.x < n_batches) issue(kb + gridDim.x, 1);
+  else if (!tma) cp_commit();
+  unsigned phase[2] = {0u, 0u};
+  int sb = 0;
+  for (; kb < n_batches; kb += gridDim.x) {
+    const long long plane0 = kb * NP;
+    const long long left = p.n_planes - plane0;
+    const int np = left < NP ? int(left) : NP;
+    float* stage = reinterpret_cast<float*>(smem_raw + L.stage[sb]);
+    if (tma) {
+      mbar_wait(&bar[sb], phase[sb]);
+      phase[sb] ^= 1u;
+    } else {
+      cp_wait<1>();
+      __syncthreads();
+    }
+    if (MODE == MODE_DZ_GELU) {  // dz = dy * gelu'(z_saved), in place
+      const float* zs = stage + NP * ZT;
+      for (int i = tid; i < np * ZT; i += nt) stage[i] *= gelu_prime_f(zs[i]);
+      fence_proxy_async();  // generic writes before the buffer is refilled by TMA
+      __syncthreads();
+    }
     // ---- phase 1: z-DFT of real columns (pencils (plane, t)) --------------
     for (int pid = tid; pid < np * T; pid += nt) {
       const int pl = pid / T, t = pid - pl * T;
       const float* col = stage + pl * ZT + t;
       float2 acc[LZ];
-      trunc_fwd<LZ>(acc, Z, p.Qz, 0, twZ, [&](int z) { return make_float2(col[z * T], 0.0f); });
+      trunc_fwd<LZ>(acc, p.Qz, twZ, [&](int z) { return make_float2(col[z * T], 0.0f); }, nk, 0);
       float2* bo = Bb + (pl * nk) * TP + t;
 #pragma unroll
       for (int j = 0; j < LZ; ++j)
         if (j < nk) bo[j * TP] = acc[j];
     }
     __syncthreads();
+    // stage buffer drained: prefetch the batch after next into it
+    const long long kn = kb + 2LL * gridDim.x;
+    if (kn < n_batches) issue(kn, sb);
+    else if (!tma) cp_commit();
     // ---- phase 2: t-DFT of complex rows (pencils (plane, kz')) ------------
     for (int pid = tid; pid < np * nk; pid += nt) {
       const int pl = pid / nk, kzp = pid - pl * nk;
       const float2* row = Bb + (pl * nk + kzp) * TP;
       float2 acc[LT];
-      trunc_fwd<LT>(acc, T, p.Qt, mt - 1, twT, [&](int t) { return row[t]; });
+      trunc_fwd<LT>(acc, p.Qt, twT, [&](int t) { return row[t]; }, mt, mt - 1);
       // plane -> (b, c, xl, yl)
       const long long plane = plane0 + pl;
       const int yl = int(plane % p.Yl);
@@ -111,15 +178,24 @@ __global__ void __launch_bounds__(256) pass_a_kernel(PassAParams p) {
         }
       }
     }
+    __syncthreads();  // Bb reused by the next batch
+    sb ^= 1;
   }
+  if (!tma) cp_wait<0>();
 }
 
-size_t pass_a_smem(int Z, int T, int mz, int NP) {
-  size_t s = (size_t(NP) * Z * T + 3) / 4 * 4 * sizeof(float);
-  s += size_t(NP) * (mz + 1) * (T + 1) * sizeof(float2);
-  s += size_t(Z + T) * sizeof(float2);
-  s += size_t(2 * mz) * sizeof(short2);
-  return s;
+void pass_a_config(int Z, int T, int mz, int mode, int* NP, size_t* smem, int* use_tma) {
+  const size_t budget = 200 * 1024;
+  int np = (AT + T - 1) / T;
+  if (np < 1) np = 1;
+  ALayout L = a_layout(Z, T, mz, np, mode);
+  while (np > 1 && L.total > budget) {
+    --np;
+    L = a_layout(Z, T, mz, np, mode);
+  }
+  *NP = np;
+  *smem = L.total;
+  *use_tma = ((size_t(Z) * T) % 4 == 0) ? 1 : 0;
 }
 
 template <int LZ, int LT>
@@ -129,7 +205,7 @@ static cudaError_t launch_a(const PassAParams& p, int mode, int grid, size_t sme
                                                 : pass_a_kernel<LZ, LT, MODE_DZ_NONE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  k<<<grid, 256, smem, st>>>(p);
+  k<<<grid, AT, smem, st>>>(p);
   return cudaGetLastError();
 }
 

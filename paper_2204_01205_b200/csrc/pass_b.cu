@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(BT) b_yfwd_kernel(PassBParams p) {
   long long* ypart = reinterpret_cast<long long*>(tw + p.Y);      // Y
   const int cm = p.C * p.nkz * p.mt;
   for (int y = threadIdx.x; y < p.Y; y += blockDim.x) ypart[y] = (long long)(y / p.Yl) * p.chunk + (long long)(y % p.Yl) * cm;
-  fill_twiddles(tw, p.Y, threadIdx.x, blockDim.x);
+  fill_combine_table(tw, L, p.Q, p.Y, p.my, -1, threadIdx.x, blockDim.x);
   __syncthreads();
   const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
   const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(BT) b_yfwd_kernel(PassBParams p) {
                           (long long)(c * p.nkz + kzl) * p.mt + kt;
   const float2* __restrict__ in = p.in;
   float2 acc[L];
-  trunc_fwd<L>(acc, p.Y, p.Q, p.my, tw, [&](int y) { return __ldg(in + xpart + ypart[y]); });
+  trunc_fwd<L>(acc, p.Q, tw, [&](int y) { return __ldg(in + xpart + ypart[y]); });
   float2* o = p.out + (((long long)(b * p.nkz + kzl) * p.C + c) * p.X + x) * (2 * p.my) * p.mt + kt;
 #pragma unroll
   for (int j = 0; j < L; ++j) {
@@ -57,7 +57,7 @@ template <int L>
 __global__ void __launch_bounds__(BT) b_xfwd_kernel(PassBParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
-  fill_twiddles(tw, p.X, threadIdx.x, blockDim.x);
+  fill_combine_table(tw, L, p.Q, p.X, p.mx, -1, threadIdx.x, blockDim.x);
   __syncthreads();
   const int my2 = 2 * p.my;
   const long long total = (long long)p.B * p.nkz * p.C * my2 * p.mt;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(BT) b_xfwd_kernel(PassBParams p) {
   const float2* __restrict__ in = p.in + ((long long)(b * p.nkz + kzl) * p.C + c) * p.X * my2 * p.mt + jy * p.mt + kt;
   const long long xs = (long long)my2 * p.mt;
   float2 acc[L];
-  trunc_fwd<L>(acc, p.X, p.Q, p.mx, tw, [&](int x) { return __ldg(in + x * xs); });
+  trunc_fwd<L>(acc, p.Q, tw, [&](int x) { return __ldg(in + x * xs); });
   const int mx2 = 2 * p.mx;
   float2* o = p.out + ((((long long)b * p.C + c) * mx2) * my2 + jy) * p.nkz * p.mt + (long long)kzl * p.mt + kt;
   const long long js = (long long)my2 * p.nkz * p.mt;
@@ -90,7 +90,7 @@ template <int L>
 __global__ void __launch_bounds__(BT) b_xinv_kernel(PassBParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
-  fill_twiddles(tw, p.X, threadIdx.x, blockDim.x);
+  fill_combine_table(tw, L, p.Q, p.X, p.mx, +1, threadIdx.x, blockDim.x);
   __syncthreads();
   const int my2 = 2 * p.my, mx2 = 2 * p.mx;
   const long long total = (long long)p.B * p.nkz * p.C * my2 * p.mt;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(BT) b_xinv_kernel(PassBParams p) {
   const long long xs = (long long)my2 * p.mt;
   for (int rc = 0; rc < p.Q; ++rc) {
     float2 y[L];
-    trunc_inv<L>(y, e, p.X, p.Q, rc, p.mx, tw);
+    trunc_inv<L>(y, e, rc, tw);
 #pragma unroll
     for (int s = 0; s < L; ++s) o[(rc + p.Q * s) * xs] = y[s];
   }
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
   long long* ypart = reinterpret_cast<long long*>(tw + p.Y);
   const int cm = p.C * p.nkz * p.mt;
   for (int y = threadIdx.x; y < p.Y; y += blockDim.x) ypart[y] = (long long)(y / p.Yl) * p.chunk + (long long)(y % p.Yl) * cm;
-  fill_twiddles(tw, p.Y, threadIdx.x, blockDim.x);
+  fill_combine_table(tw, L, p.Q, p.Y, p.my, +1, threadIdx.x, blockDim.x);
   __syncthreads();
   const int my2 = 2 * p.my;
   const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
               (long long)(oc * p.nkz + kzl) * p.mt + kt;
   for (int rc = 0; rc < p.Q; ++rc) {
     float2 y[L];
-    trunc_inv<L>(y, e, p.Y, p.Q, rc, p.my, tw);
+    trunc_inv<L>(y, e, rc, tw);
 #pragma unroll
     for (int s = 0; s < L; ++s) o[ypart[rc + p.Q * s]] = y[s];
   }

@@ -5,9 +5,12 @@
 // or, backward, dv = W^T dz + S^T dz plus the dW, db partial sums
 // (broadcast adjoint = sum-reduce).
 //
-// One CTA per (b, x, y) column (all channels).  The z outputs are produced by
-// residue class r (z = r + Qz*s, s < LZ), so a tile holds C x LZ x T values of
-// u for the 1x1 channel linear, which needs every channel at a point.
+// One persistent CTA loops over (b, x, y) columns (all channels at once: the
+// 1x1 channel linear needs every channel at a point).  The z outputs are
+// produced by residue class r (z = r + Qz*s, s < LZ) and t-chunk, so a tile is
+// C x LZ x TCH values.  Streaming is software-pipelined with cp.async: the next
+// tile's inputs (v; or dy, z, v) and the next column's spectrum are in flight
+// while the current tile is transformed and consumed.
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -16,26 +19,31 @@ namespace fno {
 static constexpr int CT = 256;  // threads per CTA
 
 struct CLayout {
-  int Cp, np, nk, TP;
-  size_t ws, bias, su, bb, vt, vt2, twz, twt, dmap, total;
+  int Cp, nk, TP, RS, NPS, NA;
+  size_t ws, bias, s, bb, u, v0, v1, twz, twt, dmap, total;
 };
 
-__host__ __device__ inline CLayout c_layout(int C, int Z, int T, int mz, int mt, int LZ, int mode) {
+__host__ __device__ inline int c_num_arrays(int mode) { return mode == EPI_U ? 0 : (mode == EPI_FWD ? 1 : 3); }
+
+// tile rows have stride RS (even, and a multiple of 4 when TCH is) so point
+// pairs and 16-byte async copies stay aligned
+__host__ __device__ inline CLayout c_layout(int C, int Z, int T, int mz, int mt, int LZ, int TCH, int mode) {
   CLayout L{};
   L.Cp = (C + 3) & ~3;
-  L.np = LZ * T;
   L.nk = mz + 1;
   L.TP = T + 1;
+  L.RS = TCH + (TCH & 1);
+  L.NPS = LZ * L.RS;
+  L.NA = c_num_arrays(mode);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
   L.ws = take(size_t(C) * L.Cp * sizeof(float));
   L.bias = take(size_t(C) * sizeof(float));
-  size_t s_bytes = size_t(C) * 2 * mz * mt * sizeof(float2);
-  size_t u_bytes = size_t(C) * L.np * sizeof(float);
-  L.su = take(s_bytes > u_bytes ? s_bytes : u_bytes);
+  L.s = take(size_t(C) * 2 * mz * mt * sizeof(float2));
   L.bb = take(size_t(C) * L.nk * L.TP * sizeof(float2));
-  L.vt = take(mode == EPI_U ? 0 : size_t(C) * L.np * sizeof(float));
-  L.vt2 = take(mode == EPI_BWD ? size_t(C) * L.np * sizeof(float) : 0);
+  L.u = take(mode == EPI_U ? 0 : size_t(C) * L.NPS * sizeof(float));
+  L.v0 = take(size_t(L.NA) * C * L.NPS * sizeof(float));
+  L.v1 = take(size_t(L.NA) * C * L.NPS * sizeof(float));
   L.twz = take(size_t(Z) * sizeof(float2));
   L.twt = take(size_t(T) * sizeof(float2));
   L.dmap = take(size_t(2 * mz) * sizeof(short2));
@@ -44,27 +52,34 @@ __host__ __device__ inline CLayout c_layout(int C, int Z, int T, int mz, int mt,
 }
 
 template <int LZ, int LT, int EPI>
-__global__ void __launch_bounds__(CT) pass_c_kernel(PassCParams p) {
+__global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
-  const CLayout L = c_layout(C, Z, T, mz, mt, LZ, EPI);
+  const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt, TCH = p.TCH;
+  const CLayout L = c_layout(C, Z, T, mz, mt, LZ, TCH, EPI);
   float* Ws = reinterpret_cast<float*>(smem_raw + L.ws);
   float* bs = reinterpret_cast<float*>(smem_raw + L.bias);
-  float2* S = reinterpret_cast<float2*>(smem_raw + L.su);
-  float* U = reinterpret_cast<float*>(smem_raw + L.su);
+  float2* S = reinterpret_cast<float2*>(smem_raw + L.s);
   float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
-  float* Vt = reinterpret_cast<float*>(smem_raw + L.vt);
-  float* Vt2 = reinterpret_cast<float*>(smem_raw + L.vt2);
+  float* U = reinterpret_cast<float*>(smem_raw + L.u);
   float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
   float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
   short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int np = L.np, nk = L.nk, TP = L.TP, Cp = L.Cp;
-  const int ZT = Z * T;
+  const int nk = L.nk, TP = L.TP, Cp = L.Cp, NPS = L.NPS, RS = L.RS;
+  constexpr int NA = (EPI == EPI_U) ? 0 : (EPI == EPI_FWD ? 1 : 3);
+  const long long ZT = (long long)Z * T;
+  const long long chan_stride = (long long)p.Xl * p.Yl * ZT;
   const int G = (C + 3) / 4;
+  const int nch = (T + TCH - 1) / TCH;
+  const int tpc = p.Qz * nch;  // tiles per column
+  const int HP = RS / 2;       // point pairs per tile row
+  const int tx = tid % HP, ty = tid / HP, TY = nt / HP;
 
-  fill_twiddles(twZ, Z, tid, nt);
-  fill_twiddles(twT, T, tid, nt);
+  long long col = blockIdx.x;
+  if (col >= p.n_cols) return;
+
+  fill_combine_table(twZ, LZ, p.Qz, Z, 0, +1, tid, nt);
+  fill_combine_table(twT, LT, p.Qt, T, mt - 1, +1, tid, nt);
   for (int j = tid; j < 2 * mz; j += nt) {
     int d = 0;
     while (j >= p.slab.kz_lo[d + 1]) ++d;
@@ -80,13 +95,62 @@ __global__ void __launch_bounds__(CT) pass_c_kernel(PassCParams p) {
     }
     for (int o = tid; o < C; o += nt) bs[o] = (EPI == EPI_FWD && p.bias) ? p.bias[o] : 0.f;
   }
+  __syncthreads();  // dmap ready for the slab loader
 
-  // dW / db accumulators (EPI_BWD): thread -> 4x4 block (og, ig) + point group
+  // ---- async loaders ---------------------------------------------------------
+  auto col_base = [&](long long c_, int* b_out) {
+    const int yl = int(c_ % p.Yl);
+    const long long r1 = c_ / p.Yl;
+    const int xl = int(r1 % p.Xl);
+    const int b = int(r1 / p.Xl);
+    *b_out = b;
+    return (long long)b * C * chan_stride + ((long long)xl * p.Yl + yl) * ZT;
+  };
+  auto issue_slab = [&](long long c_) {
+    const long long colpt = c_;  // ((b*Xl + xl)*Yl + yl) == column index
+    const int per_c = 2 * mz * mt;
+    for (int e = tid; e < C * per_c; e += nt) {
+      const int c = e / per_c, rem = e - c * per_c;
+      const int jz = rem / mt, kt = rem - jz * mt;
+      const short2 dm = dmap[jz];
+      const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
+      cp_async8(S + e, p.in + p.slab.off[dm.x] + ((colpt * C + c) * nkz + dm.y) * mt + kt);
+    }
+  };
+  auto issue_tile = [&](long long c_, int ti, int which) {
+    if (NA == 0) return;
+    float* dst = reinterpret_cast<float*>(smem_raw + (which ? L.v1 : L.v0));
+    int b;
+    const long long cb = col_base(c_, &b);
+    const int rz = ti / nch, tc = ti - rz * nch;
+    const int t0 = tc * TCH;
+    const int tcw = min(TCH, T - t0);
+    const long long base = cb + rz * T + t0;
+    const int VW = p.VW;
+    const int nvec = tcw / VW;                 // vectors per row (tcw % VW == 0 by construction)
+    const int rows = C * LZ;
+    for (int e = tid; e < rows * nvec; e += nt) {
+      const int row = e / nvec, vv = e - row * nvec;
+      const int c = row / LZ, s = row - c * LZ;
+      const long long g = base + c * chan_stride + (long long)p.Qz * s * T + vv * VW;
+      const int so = c * NPS + s * RS + vv * VW;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        const float* src = (EPI == EPI_FWD) ? p.v : (a == 0 ? p.dy : (a == 1 ? p.zs : p.v));
+        float* d = dst + a * C * NPS + so;
+        if (VW == 4) cp_async16(d, src + g);
+        else if (VW == 2) cp_async8(d, src + g);
+        else cp_async4(d, src + g);
+      }
+    }
+  };
+
+  // dW / db accumulators (EPI_BWD): thread -> 4x4 block (og, ig) + point-pair group
   const int NB = G * G;
   const int NPG = (EPI == EPI_BWD) ? max(1, nt / NB) : 1;
   const bool dw_thread = (EPI == EPI_BWD) && tid < NB * NPG;
   const int blk = tid % NB, pgrp = tid / NB;
-  const int og = blk / G, ig = blk % G;
+  const int og_w = blk / G, ig_w = blk % G;
   float dwacc[4][4];
   float dbacc[4];
 #pragma unroll
@@ -96,25 +160,17 @@ __global__ void __launch_bounds__(CT) pass_c_kernel(PassCParams p) {
     for (int c2 = 0; c2 < 4; ++c2) dwacc[a][c2] = 0.f;
   }
 
-  for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
-    const int yl = int(col % p.Yl);
-    const long long r1 = col / p.Yl;
-    const int xl = int(r1 % p.Xl);
-    const int b = int(r1 / p.Xl);
-    const long long colpt = ((long long)b * p.Xl + xl) * p.Yl + yl;
-    __syncthreads();  // previous column done with S/U/Bb/Vt; tables ready
-    // ---- phase 0: this column's retained (kz, kt) spectrum, all channels --
-    {
-      const int per_c = 2 * mz * mt;
-      for (int e = tid; e < C * per_c; e += nt) {
-        const int c = e / per_c, rem = e - c * per_c;
-        const int jz = rem / mt, kt = rem - jz * mt;
-        const short2 dm = dmap[jz];
-        const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
-        S[e] = __ldcs(p.in + p.slab.off[dm.x] + ((colpt * C + c) * nkz + dm.y) * mt + kt);
-      }
-    }
-    __syncthreads();
+  issue_slab(col);
+  cp_commit();
+  issue_tile(col, 0, 0);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  int buf = 0;
+
+  for (; col < p.n_cols; col += gridDim.x) {
+    int b;
+    const long long cbase = col_base(col, &b);
     // ---- phase 1: inverse t (C2R weights folded in), pencils (c, kz') ------
     for (int pid = tid; pid < C * nk; pid += nt) {
       const int c = pid / nk, kzp = pid - c * nk;
@@ -138,103 +194,141 @@ __global__ void __launch_bounds__(CT) pass_c_kernel(PassCParams p) {
       float2* bo = Bb + (c * nk + kzp) * TP;
       for (int rt = 0; rt < p.Qt; ++rt) {
         float2 y[LT];
-        trunc_inv<LT>(y, e, T, p.Qt, rt, mt - 1, twT);
+        trunc_inv<LT>(y, e, rt, twT);
 #pragma unroll
         for (int s = 0; s < LT; ++s) bo[rt + p.Qt * s] = y[s];
       }
     }
     __syncthreads();
-    // ---- per residue class of z ------------------------------------------
-    for (int rz = 0; rz < p.Qz; ++rz) {
-      // stage the epilogue inputs for this tile (EPI_FWD: v; EPI_BWD: dz, v)
-      if (EPI != EPI_U) {
-        for (int e = tid; e < C * np; e += nt) {
-          const int c = e / np, pt = e - c * np;
-          const int s = pt / T, t = pt - s * T;
-          const long long g = ((long long)b * C + c) * ((long long)p.Xl * p.Yl * ZT) +
-                              ((long long)xl * p.Yl + yl) * ZT + (rz + p.Qz * s) * T + t;
-          if (EPI == EPI_FWD) {
-            Vt[e] = __ldcs(p.v + g);
-          } else {
-            const float dyv = __ldcs(p.dy + g);
-            Vt[e] = p.act_gelu ? dyv * gelu_prime_f(__ldcs(p.zs + g)) : dyv;
-            Vt2[e] = __ldcs(p.v + g);
-          }
-        }
-      }
-      // phase 2: inverse z (real output), pencils (c, t)
-      for (int pid = tid; pid < C * T; pid += nt) {
-        const int c = pid / T, t = pid - c * T;
+    const long long col_next = col + gridDim.x;
+    if (col_next < p.n_cols) issue_slab(col_next);  // S is free now
+    cp_commit();
+
+    for (int ti = 0; ti < tpc; ++ti) {
+      const int rz = ti / nch, tc = ti - rz * nch;
+      const int t0 = tc * TCH;
+      const int tcw = min(TCH, T - t0);
+      if (ti + 1 < tpc) issue_tile(col, ti + 1, buf ^ 1);
+      else if (col_next < p.n_cols) issue_tile(col_next, 0, buf ^ 1);
+      cp_commit();
+      const long long tbase = cbase + rz * T + t0;   // + o*chan_stride + Qz*s*T + tt
+      // ---- phase 2: inverse z (real output) for this tile, pencils (c, tt) --
+      for (int pid = tid; pid < C * tcw; pid += nt) {
+        const int c = pid / tcw, tt = pid - c * tcw;
+        const int t = t0 + tt;
         float2 e[LZ];
 #pragma unroll
         for (int i = 0; i < LZ; ++i) e[i] = (i < nk) ? Bb[(c * nk + i) * TP + t] : make_float2(0.f, 0.f);
         float2 y[LZ];
-        trunc_inv<LZ>(y, e, Z, p.Qz, rz, 0, twZ);
+        trunc_inv<LZ>(y, e, rz, twZ);
         if (EPI == EPI_U) {
-          float* o = p.out + ((long long)b * C + c) * ((long long)p.Xl * p.Yl * ZT) + ((long long)xl * p.Yl + yl) * ZT + rz * T + t;
+          float* o = p.out + tbase + c * chan_stride + tt;
 #pragma unroll
           for (int s = 0; s < LZ; ++s) __stcs(o + (long long)p.Qz * s * T, y[s].x * p.inv_n);
         } else {
+          float* uo = U + c * NPS + tt;
 #pragma unroll
-          for (int s = 0; s < LZ; ++s) U[(c * LZ + s) * T + t] = y[s].x * p.inv_n;
+          for (int s = 0; s < LZ; ++s) uo[s * RS] = y[s].x * p.inv_n;
         }
       }
-      if (EPI == EPI_U) continue;
+      cp_wait<1>();      // this tile's inputs (and the next column's spectrum) have landed
       __syncthreads();
-      // phase 3: 1x1 channel linear + epilogue, items (o-group g, point pt)
-      for (int it = tid; it < G * np; it += nt) {
-        const int g = it / np, pt = it - g * np;
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int k = 0; k < C; ++k) {
-          const float val = Vt[k * np + pt];
-          const float4 w4 = *reinterpret_cast<const float4*>(Ws + k * Cp + 4 * g);
-          acc[0] = fmaf(w4.x, val, acc[0]);
-          acc[1] = fmaf(w4.y, val, acc[1]);
-          acc[2] = fmaf(w4.z, val, acc[2]);
-          acc[3] = fmaf(w4.w, val, acc[3]);
+      if (EPI != EPI_U) {
+        float* V = reinterpret_cast<float*>(smem_raw + (buf ? L.v1 : L.v0));
+        const bool ok0 = 2 * tx < tcw, ok1 = 2 * tx + 1 < tcw;
+        if (EPI == EPI_BWD) {
+          // dz = dy * sigma'(z) in place; zero the invalid slots so dW sees exact zeros
+          for (int r = ty; ty < TY && r < C * LZ; r += TY) {
+            float* dzr = V + r * RS + 2 * tx;
+            const float* zr = V + C * NPS + r * RS + 2 * tx;
+            float* vr = V + 2 * C * NPS + r * RS + 2 * tx;
+            float2 d2 = *reinterpret_cast<float2*>(dzr);
+            const float2 z2 = *reinterpret_cast<const float2*>(zr);
+            if (p.act_gelu) {
+              d2.x *= gelu_prime_f(z2.x);
+              d2.y *= gelu_prime_f(z2.y);
+            }
+            if (!ok0) { d2.x = 0.f; vr[0] = 0.f; }
+            if (!ok1) { d2.y = 0.f; vr[1] = 0.f; }
+            *reinterpret_cast<float2*>(dzr) = d2;
+          }
+          __syncthreads();
         }
-        const int s = pt / T, t = pt - s * T;
-        const long long gbase = ((long long)xl * p.Yl + yl) * ZT + (rz + p.Qz * s) * T + t;
+        // ---- phase 3: 1x1 channel linear + epilogue; rows (o-group, s) x pairs
+        if (ty < TY) {
+          for (int r = ty; r < G * LZ; r += TY) {
+            const int g = r / LZ, s = r - g * LZ;
+            const int p0 = s * RS + 2 * tx;
+            float acc[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+            const float* vp = V + p0;
+            const float* wp = Ws + 4 * g;
+            for (int k = 0; k < C; ++k) {
+              const float2 v2 = *reinterpret_cast<const float2*>(vp + k * NPS);
+              const float4 w4 = *reinterpret_cast<const float4*>(wp + k * Cp);
+              acc[0][0] = fmaf(w4.x, v2.x, acc[0][0]); acc[0][1] = fmaf(w4.x, v2.y, acc[0][1]);
+              acc[1][0] = fmaf(w4.y, v2.x, acc[1][0]); acc[1][1] = fmaf(w4.y, v2.y, acc[1][1]);
+              acc[2][0] = fmaf(w4.z, v2.x, acc[2][0]); acc[2][1] = fmaf(w4.z, v2.y, acc[2][1]);
+              acc[3][0] = fmaf(w4.w, v2.x, acc[3][0]); acc[3][1] = fmaf(w4.w, v2.y, acc[3][1]);
+            }
+            const long long gs = tbase + (long long)p.Qz * s * T + 2 * tx;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int o = 4 * g + a;
-          if (o < C) {
-            const long long gi = ((long long)b * C + o) * ((long long)p.Xl * p.Yl * ZT) + gbase;
-            float val = acc[a] + U[o * np + pt];
-            if (EPI == EPI_FWD) {
-              val += bs[o];
-              if (p.zsave) __stcs(p.zsave + gi, val);
-              __stcs(p.out + gi, p.act_gelu ? gelu_f(val) : val);
-            } else {
-              __stcs(p.out + gi, val);
+            for (int a = 0; a < 4; ++a) {
+              const int o = 4 * g + a;
+              if (o >= C) break;
+              const float2 u2 = *reinterpret_cast<const float2*>(U + o * NPS + p0);
+              float* out = p.out + gs + o * chan_stride;
+              float v0 = acc[a][0] + u2.x, v1 = acc[a][1] + u2.y;
+              if (EPI == EPI_FWD) {
+                v0 += bs[o];
+                v1 += bs[o];
+                if (p.zsave) {
+                  float* zo = p.zsave + gs + o * chan_stride;
+                  if (ok0) __stcs(zo, v0);
+                  if (ok1) __stcs(zo + 1, v1);
+                }
+                if (p.act_gelu) {
+                  v0 = gelu_f(v0);
+                  v1 = gelu_f(v1);
+                }
+              }
+              if (ok0) __stcs(out, v0);
+              if (ok1) __stcs(out + 1, v1);
+            }
+          }
+        }
+        if (EPI == EPI_BWD && dw_thread) {
+          const float* Dz = V;
+          const float* Vv = V + 2 * C * NPS;
+          for (int q = pgrp; q < NPS / 2; q += NPG) {
+            const int p0 = 2 * q;
+            float2 dz2[4], v2[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const int o = 4 * og_w + a, i = 4 * ig_w + a;
+              dz2[a] = (o < C) ? *reinterpret_cast<const float2*>(Dz + o * NPS + p0) : make_float2(0.f, 0.f);
+              v2[a] = (i < C) ? *reinterpret_cast<const float2*>(Vv + i * NPS + p0) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              if (ig_w == 0) dbacc[a] += dz2[a].x + dz2[a].y;
+#pragma unroll
+              for (int c2 = 0; c2 < 4; ++c2) {
+                dwacc[a][c2] = fmaf(dz2[a].x, v2[c2].x, dwacc[a][c2]);
+                dwacc[a][c2] = fmaf(dz2[a].y, v2[c2].y, dwacc[a][c2]);
+              }
             }
           }
         }
       }
-      if (EPI == EPI_BWD && dw_thread) {
-        for (int pt = pgrp; pt < np; pt += NPG) {
-          float dz4[4], v4[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int o = 4 * og + a, i = 4 * ig + a;
-            dz4[a] = (o < C) ? Vt[o * np + pt] : 0.f;
-            v4[a] = (i < C) ? Vt2[i * np + pt] : 0.f;
-          }
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            if (ig == 0) dbacc[a] += dz4[a];
-#pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2) dwacc[a][c2] = fmaf(dz4[a], v4[c2], dwacc[a][c2]);
-          }
-        }
-      }
       __syncthreads();
+      buf ^= 1;
     }
   }
+  cp_wait<0>();
   if (EPI == EPI_BWD) {
     // fixed-order CTA reduction of the per-thread partials into dWpart[blockIdx.x]
     __syncthreads();
-    float* red = Vt;  // reuse: NB*NPG*20 floats fit in the C*np tile for C >= 2
+    float* red = reinterpret_cast<float*>(smem_raw + L.v0);  // >= 20 * CT floats (host-checked)
     const int stride = 20;
     if (dw_thread) {
 #pragma unroll
@@ -258,16 +352,39 @@ __global__ void __launch_bounds__(CT) pass_c_kernel(PassCParams p) {
   }
 }
 
-size_t pass_c_smem(int C, int Z, int T, int mz, int mt, int LZ, int mode) {
-  CLayout L = c_layout(C, Z, T, mz, mt, LZ, mode);
+// smem bytes for a given chunk width; the BWD reduction reuses both V buffers
+static size_t c_smem_for(int C, int Z, int T, int mz, int mt, int LZ, int TCH, int mode) {
+  CLayout L = c_layout(C, Z, T, mz, mt, LZ, TCH, mode);
   size_t t = L.total;
   if (mode == EPI_BWD) {
-    // the final reduction reuses the Vt tile: needs 20 floats per thread
-    size_t need = size_t(CT) * 20 * sizeof(float);
-    size_t have = size_t(C) * L.np * sizeof(float);
+    const size_t need = size_t(CT) * 20 * sizeof(float);
+    const size_t have = L.total - L.v0;
     if (need > have) t += need - have;
   }
   return t;
+}
+
+void pass_c_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* TCH, int* VW, size_t* smem) {
+  const size_t budget = 227 * 1024;
+  // candidate chunks: T, then multiples of 4 (descending), then 2, 1
+  int tch = T;
+  size_t s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
+  for (int cand = (T - 1) & ~3; s > budget && cand >= 4; cand -= 4) {
+    tch = cand;
+    s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
+  }
+  for (int cand : {2, 1}) {
+    if (s <= budget) break;
+    tch = cand;
+    s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
+  }
+  int vw = 1;
+  if (T % 4 == 0 && tch % 4 == 0) vw = 4;
+  else if (T % 2 == 0 && tch % 2 == 0) vw = 2;
+  if (vw > 1 && (T % tch) % vw != 0) vw = 1;   // ragged last chunk
+  *TCH = tch;
+  *VW = vw;
+  *smem = s;
 }
 
 template <int LZ, int LT>
