@@ -132,8 +132,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned phase) {
       : "memory");
   return ok != 0;
 }
+// bounded wait: a barrier that never completes (a malformed async copy or MMA)
+// traps the kernel instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned long long spins = 0;
   while (!mbar_try_wait(bar, phase)) {
+    if (++spins > (1ull << 26)) __trap();
   }
 }
 
