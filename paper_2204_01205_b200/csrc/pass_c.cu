@@ -2,185 +2,82 @@
 // {z, t} (zero-padded inverse z, C2R along t with real-part semantics,
 // P:119-123 "F_dist^T"), fused with the DFNO block epilogue
 //   z = W v + b + u ; y = GELU(z)                      (Eq. dist_block)
-// or, backward, dv = W^T dz + S^T dz plus the dW, db sums (broadcast adjoint =
-// sum-reduce).
+// or, backward, dv = W^T dz + S^T dz plus the dW, db partial sums
+// (broadcast adjoint = sum-reduce).
 //
 // One persistent CTA loops over (b, x, y) columns (all channels at once: the
 // 1x1 channel linear needs every channel at a point).  The z outputs are
 // produced by residue class r (z = r + Qz*s, s < LZ) and t-chunk, so a tile is
-// LZ x TCH points x C channels.
-//
-// Warp specialisation (layer fwd / bwd):
-//   producer warps 0-7: per column the inverse t transform; per tile the
-//     cp.async prefetch of the next tile's inputs, the inverse z transform
-//     (-> U, the spectral part), the tf32 hi/lo split into the tensor-core
-//     operand layouts and, from one elected lane, the tcgen05.mma issue;
-//   epilogue warps 8-15: TMEM -> registers, + U + bias, GELU, stores (fwd) or
-//     dv stores and the dW/db accumulation (bwd).
-// U and the TMEM accumulators are double-buffered, so the producers transform
-// tile n+1 while the epilogue drains tile n; mbarriers (full / empty /
-// mma-done) order the two roles.
-//
-// The channel contractions are dense GEMMs on the 5th-generation tensor cores
-// (tcgen05.mma kind::tf32, accumulators in TMEM), in 3xTF32 form
-// (a_hi b_hi + a_hi b_lo + a_lo b_hi) so the result keeps fp32 accuracy:
-//   fwd:  D[point][o] = sum_i V[point][i] W[o][i]          M=128 points, N=o, K=i
-//   bwd:  D[point][i] = sum_o dz[point][o] W[o][i]         (W^T dz)
-//         D2[o][i]    = sum_points dz[point][o] v[point][i] (dW; column i=C is a
-//                       ones channel, giving db)           M=128 (o), N=i, K=points
-// Operands are K-major "interleaved" core matrices (8 rows x 16 bytes,
-// SWIZZLE_NONE), float offsets:
-//   KM  (rows = points, K = channels): ((c/4)*NBm + m/8)*32 + (m%8)*4 + (c%4)
-//   CM  (rows = channels, K = points): ((m/4)*C8 + c/8)*32 + (c%8)*4 + (m%4)
-// with NBm = points/8 and C8 = channel blocks of 8.
+// C x LZ x TCH values.  Streaming is software-pipelined with cp.async: the next
+// tile's inputs (v; or dy, z, v) and the next column's spectrum are in flight
+// while the current tile is transformed and consumed.
 #include "kernels.cuh"
 #include "launch.h"
-#include "umma.cuh"
 
 namespace fno {
 
 static constexpr int CT = 512;  // threads per CTA (16 warps)
-static constexpr int FT = 256;  // producer threads (warps 0-7)
-
-__device__ __forceinline__ void f_bar() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
 
 struct CLayout {
-  int Cp, nk, TP, RS, NPS, npad, NAR, KP, C8, N1, N2, MT, dcols, tcols;
-  size_t wb, bias, s, bb, u0, u1, r0, r1, cmv0, cmv1, kmh, kml, cmdh, cmdl, cmvl, dwacc, twz, twt, dmap, bars, tmem,
-      total;
+  int Cp, nk, TP, RS, NPS, NA;
+  size_t ws, bias, s, bb, u, v0, v1, twz, twt, dmap, total;
 };
 
+__host__ __device__ inline int c_num_arrays(int mode) { return mode == EPI_U ? 0 : (mode == EPI_FWD ? 1 : 3); }
+
+// tile rows have stride RS (even, and a multiple of 4 when TCH is) so point
+// pairs and 16-byte async copies stay aligned
 __host__ __device__ inline CLayout c_layout(int C, int Z, int T, int mz, int mt, int LZ, int TCH, int mode) {
   CLayout L{};
-  const bool tc = mode != EPI_U, bwd = mode == EPI_BWD;
   L.Cp = (C + 3) & ~3;
   L.nk = mz + 1;
   L.TP = T + 1;
-  L.RS = (TCH + 3) & ~3;                      // point-groups of 4 never straddle a z row
-  L.NPS = LZ * L.RS;                          // points per tile (incl. padding)
-  L.npad = (L.NPS + 127) & ~127;              // whole 128-row MMA tiles
-  L.MT = L.npad / 128;
-  L.NAR = mode == EPI_FWD ? 1 : (bwd ? 2 : 0);  // raw [c][point] staging arrays: v | dy, z
-  L.KP = ((C + 7) / 8) * 8;                   // K of the W GEMMs (channels, padded to 8)
-  L.C8 = (C + 1 + 7) / 8;                     // channel blocks of the CM layout (+ ones channel)
-  L.N1 = ((C + 15) / 16) * 16;                // MMA N of the W GEMMs
-  L.N2 = ((C + 1 + 15) / 16) * 16;            // MMA N of dW (incl. the ones column)
-  L.dcols = tc ? L.MT * L.N1 + (bwd ? L.N2 : 0) : 0;
-  int alloc = 32;
-  while (alloc < 2 * L.dcols) alloc *= 2;
-  L.tcols = alloc;
-  const size_t raw = size_t(C) * L.npad * sizeof(float);
-  const size_t km = size_t(L.npad) * L.KP * sizeof(float);
-  const size_t cm = size_t(L.npad) * L.C8 * 8 * sizeof(float);
+  L.RS = TCH + (TCH & 1);
+  L.NPS = LZ * L.RS;
+  L.NA = c_num_arrays(mode);
   size_t off = 0;
-  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 127) & ~size_t(127); return o; };
-  L.wb = take(tc ? 2 * size_t(L.N1) * L.KP * sizeof(float) : 0);   // B hi, lo (K-major)
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
+  L.ws = take(size_t(C) * L.Cp * sizeof(float));
   L.bias = take(size_t(C) * sizeof(float));
   L.s = take(size_t(C) * 2 * mz * mt * sizeof(float2));
   L.bb = take(size_t(C) * L.nk * L.TP * sizeof(float2));
-  L.kmh = take(tc ? km : 0);
-  L.kml = take(tc ? km : 0);
-  L.cmdh = take(bwd ? cm : 0);
-  L.cmdl = take(bwd ? cm : 0);
-  L.cmvl = take(bwd ? cm : 0);
-  L.cmv0 = take(bwd ? cm : 0);
-  L.cmv1 = take(bwd ? cm : 0);
-  L.u0 = take(tc ? size_t(C) * L.npad * sizeof(float) : 0);   // after the CM buffers: dW descriptors
-  L.u1 = take(tc ? size_t(C) * L.npad * sizeof(float) : 0);   // may read a little past them
-  L.r0 = take(size_t(L.NAR) * raw);
-  L.r1 = take(size_t(L.NAR) * raw);
-  L.dwacc = take(bwd ? size_t(C) * L.N2 * sizeof(float) : 0);
+  L.u = take(mode == EPI_U ? 0 : size_t(C) * L.NPS * sizeof(float));
+  L.v0 = take(size_t(L.NA) * C * L.NPS * sizeof(float));
+  L.v1 = take(size_t(L.NA) * C * L.NPS * sizeof(float));
   L.twz = take(size_t(Z) * sizeof(float2));
   L.twt = take(size_t(T) * sizeof(float2));
   L.dmap = take(size_t(2 * mz) * sizeof(short2));
-  L.bars = take(6 * sizeof(uint64_t));
-  L.tmem = take(sizeof(uint32_t));
   L.total = off;
   return L;
 }
 
-// per-column phase 1: inverse t with the C2R weights folded in, pencils (c, kz')
-template <int LT>
-__device__ __forceinline__ void phase1(const float2* S, float2* Bb, const float2* twT, int C, int T, int mz, int mt,
-                                       int nk, int TP, int Qt, int tid, int nthr) {
-  for (int pid = tid; pid < C * nk; pid += nthr) {
-    const int c = pid / nk, kzp = pid - c * nk;
-    const float2* Sp = S + (c * 2 * mz + kzp) * mt;              // kz = +kz'
-    const float2* Sn = S + (c * 2 * mz + (2 * mz - kzp)) * mt;   // kz = -kz'
-    float2 e[LT];
-#pragma unroll
-    for (int i = 0; i < LT; ++i) {
-      float2 acc = make_float2(0.f, 0.f);
-      if (i < mt && kzp < mz) {
-        const float cw = (i == 0 || 2 * i == T) ? 1.f : 2.f;
-        acc = cscale(Sp[i], cw);
-      }
-      const int kt = (LT - i) % LT;
-      if (kzp >= 1 && kt < mt && (i == 0 || i > LT - mt)) {
-        const float cw = (kt == 0 || 2 * kt == T) ? 1.f : 2.f;
-        acc = cadd(acc, cscale(cconj(Sn[kt]), cw));
-      }
-      e[i] = acc;
-    }
-    float2* bo = Bb + (c * nk + kzp) * TP;
-    for (int rt = 0; rt < Qt; ++rt) {
-      float2 y[LT];
-      trunc_inv<LT>(y, e, rt, twT);
-#pragma unroll
-      for (int s = 0; s < LT; ++s) bo[rt + Qt * s] = y[s];
-    }
-  }
-}
-
-// column index -> NCXYZT offset of (b, c=0, xl, yl, z=0, t=0)
-__device__ __forceinline__ long long col_base_of(const PassCParams& p, long long c_, long long ZT, long long chan_stride) {
-  const unsigned cu = unsigned(c_);            // n_cols < 2^31 (checked by the plan)
-  const unsigned yl = cu % unsigned(p.Yl);
-  const unsigned r1 = cu / unsigned(p.Yl);
-  const unsigned xl = r1 % unsigned(p.Xl);
-  const unsigned b = r1 / unsigned(p.Xl);
-  return (long long)b * p.C * chan_stride + ((long long)xl * p.Yl + yl) * ZT;
-}
-
-__device__ __forceinline__ void issue_slab(const PassCParams& p, float2* S, const short2* dmap, long long colpt, int C,
-                                           int mz, int mt, int tid, int nthr) {
-  const int per_c = 2 * mz * mt;
-  if (p.slab.P == 1 && (per_c & 1) == 0) {   // one owner: a contiguous run of C*2mz*mt complex
-    const float2* src = p.in + colpt * C * per_c;
-    for (int e = tid; e < C * per_c / 2; e += nthr) cp_async16(S + 2 * e, src + 2 * e);
-    return;
-  }
-  for (int e = tid; e < C * per_c; e += nthr) {
-    const int c = e / per_c, rem = e - c * per_c;
-    const int jz = rem / mt, kt = rem - jz * mt;
-    const short2 dm = dmap[jz];
-    const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
-    cp_async8(S + e, p.in + p.slab.off[dm.x] + ((colpt * C + c) * nkz + dm.y) * mt + kt);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// spectral convolution only (u = S v): no channel contraction, all warps
-// ---------------------------------------------------------------------------
-template <int LZ, int LT>
-__global__ void __launch_bounds__(CT, 1) pass_c_u_kernel(PassCParams p) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
-  const CLayout L = c_layout(C, Z, T, mz, mt, LZ, T, EPI_U);
+template <int LZ, int LT, int EPI>
+__global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt, TCH = p.TCH;
+  const CLayout L = c_layout(C, Z, T, mz, mt, LZ, TCH, EPI);
+  float* Ws = reinterpret_cast<float*>(smem_raw + L.ws);
+  float* bs = reinterpret_cast<float*>(smem_raw + L.bias);
   float2* S = reinterpret_cast<float2*>(smem_raw + L.s);
   float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
+  float* U = reinterpret_cast<float*>(smem_raw + L.u);
   float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
   float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
   short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int nk = L.nk, TP = L.TP;
+  const int nk = L.nk, TP = L.TP, Cp = L.Cp, NPS = L.NPS, RS = L.RS;
+  constexpr int NA = (EPI == EPI_U) ? 0 : (EPI == EPI_FWD ? 1 : 3);
   const long long ZT = (long long)Z * T;
   const long long chan_stride = (long long)p.Xl * p.Yl * ZT;
+  const int G = (C + 3) / 4;
+  const int nch = (T + TCH - 1) / TCH;
+  const int tpc = p.Qz * nch;  // tiles per column
+  const int HP = RS / 2;       // point pairs per tile row
+  const int tx = tid % HP, ty = tid / HP, TY = nt / HP;
+
   long long col = blockIdx.x;
   if (col >= p.n_cols) return;
+
   fill_combine_table(twZ, LZ, p.Qz, Z, 0, +1, tid, nt);
   fill_combine_table(twT, LT, p.Qt, T, mt - 1, +1, tid, nt);
   for (int j = tid; j < 2 * mz; j += nt) {
@@ -188,420 +85,307 @@ __global__ void __launch_bounds__(CT, 1) pass_c_u_kernel(PassCParams p) {
     while (j >= p.slab.kz_lo[d + 1]) ++d;
     dmap[j] = make_short2(short(d), short(j - p.slab.kz_lo[d]));
   }
-  __syncthreads();
-  issue_slab(p, S, dmap, col, C, mz, mt, tid, nt);
+  if (EPI != EPI_U) {
+    // Ws[k*Cp + out]: fwd k = input channel (W^T), bwd k = output channel (W)
+    for (int e = tid; e < C * Cp; e += nt) {
+      const int k = e / Cp, o = e - k * Cp;
+      float w = 0.f;
+      if (o < C) w = (EPI == EPI_FWD) ? p.W[o * C + k] : p.W[k * C + o];
+      Ws[e] = w;
+    }
+    for (int o = tid; o < C; o += nt) bs[o] = (EPI == EPI_FWD && p.bias) ? p.bias[o] : 0.f;
+  }
+  __syncthreads();  // dmap ready for the slab loader
+
+  // ---- async loaders ---------------------------------------------------------
+  auto col_base = [&](long long c_, int* b_out) {
+    const unsigned cu = unsigned(c_);          // n_cols < 2^31 (checked by the plan)
+    const unsigned yl = cu % unsigned(p.Yl);
+    const unsigned r1 = cu / unsigned(p.Yl);
+    const unsigned xl = r1 % unsigned(p.Xl);
+    const int b = int(r1 / unsigned(p.Xl));
+    *b_out = b;
+    return (long long)b * C * chan_stride + ((long long)xl * p.Yl + yl) * ZT;
+  };
+  auto issue_slab = [&](long long c_) {
+    const long long colpt = c_;  // ((b*Xl + xl)*Yl + yl) == column index
+    const int per_c = 2 * mz * mt;
+    if (p.slab.P == 1 && (per_c & 1) == 0) {   // one owner: a contiguous run of C*2mz*mt complex
+      const float2* src = p.in + colpt * C * per_c;
+      for (int e = tid; e < C * per_c / 2; e += nt) cp_async16(S + 2 * e, src + 2 * e);
+      return;
+    }
+    for (int e = tid; e < C * per_c; e += nt) {
+      const int c = e / per_c, rem = e - c * per_c;
+      const int jz = rem / mt, kt = rem - jz * mt;
+      const short2 dm = dmap[jz];
+      const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
+      cp_async8(S + e, p.in + p.slab.off[dm.x] + ((colpt * C + c) * nkz + dm.y) * mt + kt);
+    }
+  };
+  auto issue_tile = [&](long long cb, int ti, int which) {
+    if (NA == 0) return;
+    float* dst = reinterpret_cast<float*>(smem_raw + (which ? L.v1 : L.v0));
+    const int rz = ti / nch, tc = ti - rz * nch;
+    const int t0 = tc * TCH;
+    const int tcw = min(TCH, T - t0);
+    const long long base = cb + rz * T + t0;
+    const int VW = p.VW;
+    const int nvec = tcw / VW;                 // vectors per row (tcw % VW == 0 by construction)
+    const int rows = C * LZ;
+    const int vv = tid % nvec, rstep = nt / nvec;
+    for (int row = tid / nvec; row < rows; row += rstep) {
+      const int c = row / LZ, s = row - c * LZ;
+      const long long g = base + c * chan_stride + (long long)p.Qz * s * T + vv * VW;
+      const int so = c * NPS + s * RS + vv * VW;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        const float* src = (EPI == EPI_FWD) ? p.v : (a == 0 ? p.dy : (a == 1 ? p.zs : p.v));
+        float* d = dst + a * C * NPS + so;
+        if (VW == 4) cp_async16(d, src + g);
+        else if (VW == 2) cp_async8(d, src + g);
+        else cp_async4(d, src + g);
+      }
+    }
+  };
+
+  // dW / db accumulators (EPI_BWD): thread -> 4x4 block (og, ig) + point-pair group
+  const int NB = G * G;
+  const int NPG = (EPI == EPI_BWD) ? max(1, nt / NB) : 1;
+  const bool dw_thread = (EPI == EPI_BWD) && tid < NB * NPG;
+  const int blk = tid % NB, pgrp = tid / NB;
+  const int og_w = blk / G, ig_w = blk % G;
+  float dwacc[4][4];
+  float dbacc[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    dbacc[a] = 0.f;
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) dwacc[a][c2] = 0.f;
+  }
+
+  issue_slab(col);
   cp_commit();
+  {
+    int b0;
+    issue_tile(col_base(col, &b0), 0, 0);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  int buf = 0;
+
   for (; col < p.n_cols; col += gridDim.x) {
-    cp_wait<0>();
-    __syncthreads();
-    phase1<LT>(S, Bb, twT, C, T, mz, mt, nk, TP, p.Qt, tid, nt);
+    int b;
+    const long long cbase = col_base(col, &b);
+    // ---- phase 1: inverse t (C2R weights folded in), pencils (c, kz') ------
+    for (int pid = tid; pid < C * nk; pid += nt) {
+      const int c = pid / nk, kzp = pid - c * nk;
+      const float2* Sp = S + (c * 2 * mz + kzp) * mt;              // kz = +kz'
+      const float2* Sn = S + (c * 2 * mz + (2 * mz - kzp)) * mt;   // kz = -kz'
+      float2 e[LT];
+#pragma unroll
+      for (int i = 0; i < LT; ++i) {
+        float2 acc = make_float2(0.f, 0.f);
+        if (i < mt && kzp < mz) {
+          const float cw = (i == 0 || 2 * i == T) ? 1.f : 2.f;
+          acc = cscale(Sp[i], cw);
+        }
+        const int kt = (LT - i) % LT;
+        if (kzp >= 1 && kt < mt && (i == 0 || i > LT - mt)) {
+          const float cw = (kt == 0 || 2 * kt == T) ? 1.f : 2.f;
+          acc = cadd(acc, cscale(cconj(Sn[kt]), cw));
+        }
+        e[i] = acc;
+      }
+      float2* bo = Bb + (c * nk + kzp) * TP;
+      for (int rt = 0; rt < p.Qt; ++rt) {
+        float2 y[LT];
+        trunc_inv<LT>(y, e, rt, twT);
+#pragma unroll
+        for (int s = 0; s < LT; ++s) bo[rt + p.Qt * s] = y[s];
+      }
+    }
     __syncthreads();
     const long long col_next = col + gridDim.x;
-    if (col_next < p.n_cols) issue_slab(p, S, dmap, col_next, C, mz, mt, tid, nt);
+    int bnext = 0;
+    const long long cbase_next = col_next < p.n_cols ? col_base(col_next, &bnext) : 0;
+    if (col_next < p.n_cols) issue_slab(col_next);  // S is free now
     cp_commit();
-    const long long cbase = col_base_of(p, col, ZT, chan_stride);
-    for (int rz = 0; rz < p.Qz; ++rz) {
-      for (int pid = tid; pid < C * T; pid += nt) {
-        const int c = pid / T, t = pid - c * T;
+
+    for (int ti = 0; ti < tpc; ++ti) {
+      const int rz = ti / nch, tc = ti - rz * nch;
+      const int t0 = tc * TCH;
+      const int tcw = min(TCH, T - t0);
+      if (ti + 1 < tpc) issue_tile(cbase, ti + 1, buf ^ 1);
+      else if (col_next < p.n_cols) issue_tile(cbase_next, 0, buf ^ 1);
+      cp_commit();
+      const long long tbase = cbase + rz * T + t0;   // + o*chan_stride + Qz*s*T + tt
+      // ---- phase 2: inverse z (real output) for this tile, pencils (c, tt) --
+      for (int pid = tid; pid < C * tcw; pid += nt) {
+        const int c = pid / tcw, tt = pid - c * tcw;
+        const int t = t0 + tt;
         float2 e[LZ];
 #pragma unroll
         for (int i = 0; i < LZ; ++i) e[i] = (i < nk) ? Bb[(c * nk + i) * TP + t] : make_float2(0.f, 0.f);
         float2 y[LZ];
         trunc_inv<LZ>(y, e, rz, twZ);
-        float* o = p.out + cbase + c * chan_stride + rz * T + t;
+        if (EPI == EPI_U) {
+          float* o = p.out + tbase + c * chan_stride + tt;
 #pragma unroll
-        for (int s = 0; s < LZ; ++s) __stcs(o + (long long)p.Qz * s * T, y[s].x * p.inv_n);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// DFNO block forward / backward with tensor-core channel contractions
-// ---------------------------------------------------------------------------
-template <int LZ, int LT, int EPI>
-__global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt, TCH = p.TCH;
-  const CLayout L = c_layout(C, Z, T, mz, mt, LZ, TCH, EPI);
-  constexpr bool BWD = (EPI == EPI_BWD);
-  float* WB = reinterpret_cast<float*>(smem_raw + L.wb);
-  float* bs = reinterpret_cast<float*>(smem_raw + L.bias);
-  float2* S = reinterpret_cast<float2*>(smem_raw + L.s);
-  float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
-  float* KMH = reinterpret_cast<float*>(smem_raw + L.kmh);
-  float* KML = reinterpret_cast<float*>(smem_raw + L.kml);
-  float* CMDH = reinterpret_cast<float*>(smem_raw + L.cmdh);
-  float* CMDL = reinterpret_cast<float*>(smem_raw + L.cmdl);
-  float* CMVL = reinterpret_cast<float*>(smem_raw + L.cmvl);
-  float* DWA = reinterpret_cast<float*>(smem_raw + L.dwacc);   // [C][N2] fp32 dW/db accumulator
-  float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
-  float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
-  short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bars);   // full[2], empty[2], mma[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + L.tmem);
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int nk = L.nk, TP = L.TP, RS = L.RS, NPS = L.NPS, C8 = L.C8, KP = L.KP, npad = L.npad, MT = L.MT;
-  const int NBm = npad / 8;
-  const long long ZT = (long long)Z * T;
-  const long long chan_stride = (long long)p.Xl * p.Yl * ZT;
-  const int nch = (T + TCH - 1) / TCH;
-  const int tpc = p.Qz * nch;  // tiles per column
-
-  const long long col0 = blockIdx.x;
-  if (col0 >= p.n_cols) return;
-
-  // ---- setup (all warps) -------------------------------------------------------
-  fill_combine_table(twZ, LZ, p.Qz, Z, 0, +1, tid, CT);
-  fill_combine_table(twT, LT, p.Qt, T, mt - 1, +1, tid, CT);
-  for (int j = tid; j < 2 * mz; j += CT) {
-    int d = 0;
-    while (j >= p.slab.kz_lo[d + 1]) ++d;
-    dmap[j] = make_short2(short(d), short(j - p.slab.kz_lo[d]));
-  }
-  for (int o = tid; o < C; o += CT) bs[o] = (EPI == EPI_FWD && p.bias) ? p.bias[o] : 0.f;
-  {
-    // B operand of the W GEMM, K-major interleaved: element (n, k) at
-    // ((k/4)*(N1/8) + n/8)*32 + (n%8)*4 + (k%4); fwd B[n=o][k=i] = W[o][i],
-    // bwd B[n=i][k=o] = W[o][i]; hi and lo parts for 3xTF32
-    const int nb8 = L.N1 / 8;
-    const int bfl = L.N1 * KP;
-    for (int e = tid; e < bfl; e += CT) {
-      const int kc = e / (nb8 * 32), r = e - kc * nb8 * 32;
-      const int nb = r / 32, r2 = r - nb * 32;
-      const int n = nb * 8 + r2 / 4, k = kc * 4 + (r2 & 3);
-      float w = 0.f;
-      if (n < C && k < C) w = (EPI == EPI_FWD) ? p.W[n * C + k] : p.W[k * C + n];
-      const float hi = tf32_hi(w);
-      WB[e] = hi;
-      WB[bfl + e] = w - hi;
-    }
-  }
-  {
-    // zero the operand and staging buffers once: padded channels stay zero
-    float* z0 = reinterpret_cast<float*>(smem_raw + L.kmh);
-    const size_t nz = (L.twz - L.kmh) / sizeof(float);
-    for (size_t e = tid; e < nz; e += CT) z0[e] = 0.f;
-  }
-  if (warp == 0) tmem_alloc(tmem_slot, L.tcols);
-  if (tid == 0) {
-    mbar_init(&bars[0], FT);  // full[0]
-    mbar_init(&bars[1], FT);  // full[1]
-    mbar_init(&bars[2], FT);  // empty[0]
-    mbar_init(&bars[3], FT);  // empty[1]
-    mbar_init(&bars[4], 1);   // mma[0]
-    mbar_init(&bars[5], 1);   // mma[1]
-    mbar_fence_init();
-  }
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp < 8) {
-    // =========================== producer warps ===============================
-    const int ft = tid;
-    // tile inputs: part 0 = the raw [c][point] staging arrays (v | dy, z);
-    // part 1 = v in the CM operand layout (bwd; read by the dW MMA, so it is
-    // only refilled after that MMA has completed)
-    auto issue_tile = [&](long long cb, int ti, int b, int part) {
-      if (part == 1 && !BWD) return;
-      float* raw = reinterpret_cast<float*>(smem_raw + (b ? L.r1 : L.r0));
-      float* cmv = reinterpret_cast<float*>(smem_raw + (b ? L.cmv1 : L.cmv0));
-      const int rz = ti / nch, tc = ti - rz * nch;
-      const int t0 = tc * TCH;
-      const int tcw = min(TCH, T - t0);
-      const long long base = cb + rz * T + t0;
-      const int VW = p.VW;
-      const int nvec = tcw / VW;                 // vectors per row (tcw % VW == 0 by construction)
-      const int vv = ft % nvec, rstep = FT / nvec;
-      for (int row = ft / nvec; row < C * LZ; row += rstep) {
-        const int c = row / LZ, s = row - c * LZ;
-        const long long g = base + c * chan_stride + (long long)p.Qz * s * T + vv * VW;
-        const int m = s * RS + vv * VW;
-        if (part == 0) {
-          float* d0 = raw + c * npad + m;
-          const float* s0 = BWD ? p.dy : p.v;
-          if (VW == 4) cp_async16(d0, s0 + g);
-          else if (VW == 2) cp_async8(d0, s0 + g);
-          else cp_async4(d0, s0 + g);
-          if (BWD) {
-            float* d1 = raw + C * npad + c * npad + m;
-            if (VW == 4) cp_async16(d1, p.zs + g);
-            else if (VW == 2) cp_async8(d1, p.zs + g);
-            else cp_async4(d1, p.zs + g);
-          }
+          for (int s = 0; s < LZ; ++s) __stcs(o + (long long)p.Qz * s * T, y[s].x * p.inv_n);
         } else {
-          float* d2 = cmv + ((m >> 2) * C8 + (c >> 3)) * 32 + (c & 7) * 4 + (m & 3);
-          if (VW == 4) cp_async16(d2, p.v + g);
-          else if (VW == 2) cp_async8(d2, p.v + g);
-          else cp_async4(d2, p.v + g);
-        }
-      }
-    };
-
-    issue_slab(p, S, dmap, col0, C, mz, mt, ft, FT);
-    cp_commit();
-    issue_tile(col_base_of(p, col0, ZT, chan_stride), 0, 0, 0);
-    issue_tile(col_base_of(p, col0, ZT, chan_stride), 0, 0, 1);
-    cp_commit();
-    cp_wait<1>();  // S(col0)
-    f_bar();
-    int n = 0;     // tile sequence number of this CTA
-    for (long long col = col0; col < p.n_cols; col += gridDim.x) {
-      phase1<LT>(S, Bb, twT, C, T, mz, mt, nk, TP, p.Qt, ft, FT);
-      f_bar();
-      const long long cbase = col_base_of(p, col, ZT, chan_stride);
-      const long long col_next = col + gridDim.x;
-      const long long cbase_next = col_next < p.n_cols ? col_base_of(p, col_next, ZT, chan_stride) : 0;
-      if (col_next < p.n_cols) issue_slab(p, S, dmap, col_next, C, mz, mt, ft, FT);  // S is free now
-      cp_commit();
-      for (int ti = 0; ti < tpc; ++ti, ++n) {
-        const int b = n & 1;
-        const int rz = ti / nch, tc = ti - rz * nch;
-        const int t0 = tc * TCH;
-        const int tcw = min(TCH, T - t0);
-        const bool has_next = (ti + 1 < tpc) || (col_next < p.n_cols);
-        const long long nb_base = (ti + 1 < tpc) ? cbase : cbase_next;
-        const int nb_ti = (ti + 1 < tpc) ? ti + 1 : 0;
-        if (has_next) issue_tile(nb_base, nb_ti, b ^ 1, 0);
-        cp_commit();
-        if (n >= 2) mbar_wait(&bars[2 + b], ((n - 2) >> 1) & 1);   // epilogue done with U[b], D[b]
-        // ---- inverse z (real output) -> U[b], pencils (c, tt) ----------------
-        float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
-        for (int pid = ft; pid < C * tcw; pid += FT) {
-          const int c = pid / tcw, tt = pid - c * tcw;
-          const int t = t0 + tt;
-          float2 e[LZ];
-#pragma unroll
-          for (int i = 0; i < LZ; ++i) e[i] = (i < nk) ? Bb[(c * nk + i) * TP + t] : make_float2(0.f, 0.f);
-          float2 y[LZ];
-          trunc_inv<LZ>(y, e, rz, twZ);
-          float* uo = U + c * npad + tt;
+          float* uo = U + c * NPS + tt;
 #pragma unroll
           for (int s = 0; s < LZ; ++s) uo[s * RS] = y[s].x * p.inv_n;
         }
-        cp_wait<1>();                       // this tile's inputs (and the next spectrum) landed
-        if (n >= 1) mbar_wait(&bars[4 + (b ^ 1)], ((n - 1) >> 1) & 1);   // MMAs of tile n-1 done
-        if (has_next) issue_tile(nb_base, nb_ti, b ^ 1, 1);             // v of tile n+1 -> CM[b^1]
-        cp_commit();
-        f_bar();
-        // ---- tf32 hi/lo split + layout change (bwd: dz, invalid points, ones) --
-        const float* R0 = reinterpret_cast<const float*>(smem_raw + (b ? L.r1 : L.r0));
-        float* CMV = reinterpret_cast<float*>(smem_raw + (b ? L.cmv1 : L.cmv0));
-        const int nc4 = BWD ? (C + 1 + 3) / 4 : (C + 3) / 4;
-        for (int it = ft; it < (npad / 4) * nc4; it += FT) {
-          const int g = it / nc4, cc = it - g * nc4;
-          const int m0 = 4 * g;
-          bool ok[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int m = m0 + j;
-            const int s = m / RS, tt = m - s * RS;
-            ok[j] = (m < NPS) && (tt < tcw);
-          }
-          float a[4][4];   // [channel j][point i]: v (fwd) or dz (bwd)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int c = 4 * cc + j;
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f), zz = x;
-            if (c < C) {
-              x = *reinterpret_cast<const float4*>(R0 + c * npad + m0);
-              if (BWD) zz = *reinterpret_cast<const float4*>(R0 + C * npad + c * npad + m0);
-            }
-            const float xs[4] = {x.x, x.y, x.z, x.w}, zs4[4] = {zz.x, zz.y, zz.z, zz.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (!BWD) a[j][i] = xs[i];
-              else a[j][i] = (c < C && ok[i]) ? (p.act_gelu ? xs[i] * gelu_prime_f(zs4[i]) : xs[i]) : 0.f;
-            }
-          }
-          if (4 * cc < KP) {   // KM (rows = points): A of the W GEMM
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int m = m0 + i;
-              const int off = (cc * NBm + (m >> 3)) * 32 + (m & 7) * 4;
-              float h[4], l[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                h[j] = tf32_hi(a[j][i]);
-                l[j] = a[j][i] - h[j];
-              }
-              *reinterpret_cast<float4*>(KMH + off) = make_float4(h[0], h[1], h[2], h[3]);
-              *reinterpret_cast<float4*>(KML + off) = make_float4(l[0], l[1], l[2], l[3]);
-            }
-          }
-          if (BWD) {  // CM (rows = channels): dW GEMM operands dz (A) and v (B, hi in place)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int c = 4 * cc + j;
-              if (c >= 8 * C8) continue;
-              const int off = (g * C8 + (c >> 3)) * 32 + (c & 7) * 4;
-              float4 v4 = *reinterpret_cast<const float4*>(CMV + off);
-              const float vin[4] = {v4.x, v4.y, v4.z, v4.w};
-              float dh[4], dl[4], vh[4], vl[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                dh[i] = tf32_hi(a[j][i]);
-                dl[i] = a[j][i] - dh[i];
-                const float vv = (c < C) ? (ok[i] ? vin[i] : 0.f) : ((c == C && ok[i]) ? 1.f : 0.f);
-                vh[i] = tf32_hi(vv);
-                vl[i] = vv - vh[i];
-              }
-              *reinterpret_cast<float4*>(CMDH + off) = make_float4(dh[0], dh[1], dh[2], dh[3]);
-              *reinterpret_cast<float4*>(CMDL + off) = make_float4(dl[0], dl[1], dl[2], dl[3]);
-              *reinterpret_cast<float4*>(CMV + off) = make_float4(vh[0], vh[1], vh[2], vh[3]);
-              *reinterpret_cast<float4*>(CMVL + off) = make_float4(vl[0], vl[1], vl[2], vl[3]);
-            }
-          }
-        }
-        fence_proxy_async();   // generic smem writes -> visible to the tensor core (async proxy)
-        mbar_arrive(&bars[b]); // full[b]: U[b] is written
-        f_bar();
-        // ---- tcgen05.mma from one elected lane of warp 0 --------------------
-        if (warp == 0) {
-          tc_fence_after();
-          const bool leader = elect_one();
-          const uint32_t dbase = tmem + b * L.dcols;
-          const uint32_t idesc1 = umma_idesc_tf32(128, L.N1, 0, 0);
-          const uint32_t lboA = NBm * 128;            // K-major A: 4-channel chunk stride
-          const uint32_t lboB = (L.N1 / 8) * 128;     // K-major B: 4-channel chunk stride
-          for (int m4 = 0; m4 < MT; ++m4) {
-            for (int ks = 0; ks < KP / 8; ++ks) {
-              const int ao = m4 * 16 * 32 + ks * 2 * NBm * 32;            // floats
-              const uint64_t ah = umma_sdesc(KMH + ao, lboA, 128);
-              const uint64_t al = umma_sdesc(KML + ao, lboA, 128);
-              const uint64_t bh = umma_sdesc(WB + ks * 2 * (lboB / 4), lboB, 128);
-              const uint64_t bl = umma_sdesc(WB + L.N1 * KP + ks * 2 * (lboB / 4), lboB, 128);
-              if (leader) {
-                umma_tf32(dbase + m4 * L.N1, ah, bh, idesc1, ks > 0 ? 1u : 0u);
-                umma_tf32(dbase + m4 * L.N1, ah, bl, idesc1, 1u);
-                umma_tf32(dbase + m4 * L.N1, al, bh, idesc1, 1u);
-              }
-            }
-          }
-          if (BWD) {
-            const uint32_t idesc2 = umma_idesc_tf32(128, L.N2, 0, 0);
-            const uint32_t d2 = dbase + MT * L.N1;
-            for (int ks = 0; ks < npad / 8; ++ks) {
-              const int ko = ks * 2 * C8 * 32;                              // 8 points = 2 groups
-              const uint64_t ah = umma_sdesc(CMDH + ko, C8 * 128, 128);
-              const uint64_t al = umma_sdesc(CMDL + ko, C8 * 128, 128);
-              const uint64_t bh = umma_sdesc(CMV + ko, C8 * 128, 128);
-              const uint64_t bl = umma_sdesc(CMVL + ko, C8 * 128, 128);
-              if (leader) {
-                umma_tf32(d2, ah, bh, idesc2, ks > 0 ? 1u : 0u);   // fresh per tile
-                umma_tf32(d2, ah, bl, idesc2, 1u);
-                umma_tf32(d2, al, bh, idesc2, 1u);
-              }
-            }
-          }
-          __syncwarp();
-          if (leader) umma_commit(&bars[4 + b]);
-        }
       }
-    }
-    cp_wait<0>();
-  } else {
-    // =========================== epilogue warps ===============================
-    const int q = warp & 3;          // TMEM lane quadrant (== warp % 4)
-    const int h = (warp - 8) >> 2;   // two epilogue warps per quadrant split the output columns
-    int n = 0;
-    for (long long col = col0; col < p.n_cols; col += gridDim.x) {
-      const long long cbase = col_base_of(p, col, ZT, chan_stride);
-      for (int ti = 0; ti < tpc; ++ti, ++n) {
-        const int b = n & 1;
-        const int rz = ti / nch, tc = ti - rz * nch;
-        const int t0 = tc * TCH;
-        const int tcw = min(TCH, T - t0);
-        const long long tbase = cbase + rz * T + t0;
-        mbar_wait(&bars[b], (n >> 1) & 1);       // U[b] written
-        mbar_wait(&bars[4 + b], (n >> 1) & 1);   // MMAs of tile n done
-        tc_fence_after();
-        const float* U = reinterpret_cast<const float*>(smem_raw + (b ? L.u1 : L.u0));
-        const uint32_t dbase = tmem + b * L.dcols + ((uint32_t)(32 * q) << 16);
-        for (int m4 = 0; m4 < MT; ++m4) {
-          const int m = m4 * 128 + 32 * q + lane;
-          const int s = m / RS, tt = m - s * RS;
-          const bool okp = (m < NPS) && (tt < tcw);
-          const long long gs = tbase + (long long)p.Qz * s * T + tt;
-          for (int c0 = 8 * h; c0 < C; c0 += 16) {
-            float d8[8];
-            tmem_ld8(dbase + m4 * L.N1 + c0, d8);
-            if (!okp) continue;
+      cp_wait<1>();      // this tile's inputs (and the next column's spectrum) have landed
+      __syncthreads();
+      if (EPI != EPI_U) {
+        float* V = reinterpret_cast<float*>(smem_raw + (buf ? L.v1 : L.v0));
+        const bool ok0 = 2 * tx < tcw, ok1 = 2 * tx + 1 < tcw;
+        if (EPI == EPI_BWD) {
+          // dz = dy * sigma'(z) in place; zero the invalid slots so dW sees exact zeros
+          for (int r = ty; ty < TY && r < C * LZ; r += TY) {
+            float* dzr = V + r * RS + 2 * tx;
+            const float* zr = V + C * NPS + r * RS + 2 * tx;
+            float* vr = V + 2 * C * NPS + r * RS + 2 * tx;
+            float2 d2 = *reinterpret_cast<float2*>(dzr);
+            const float2 z2 = *reinterpret_cast<const float2*>(zr);
+            if (p.act_gelu) {
+              d2.x *= gelu_prime_f(z2.x);
+              d2.y *= gelu_prime_f(z2.y);
+            }
+            if (!ok0) { d2.x = 0.f; vr[0] = 0.f; }
+            if (!ok1) { d2.y = 0.f; vr[1] = 0.f; }
+            *reinterpret_cast<float2*>(dzr) = d2;
+          }
+          __syncthreads();
+        }
+        // ---- phase 3: 1x1 channel linear + epilogue; rows (o-group, s) x pairs
+        if (ty < TY) {
+          for (int r = ty; r < G * LZ; r += TY) {
+            const int g = r / LZ, s = r - g * LZ;
+            const int p0 = s * RS + 2 * tx;
+            float acc[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+            const float* vp = V + p0;
+            const float* wp = Ws + 4 * g;
+            for (int k = 0; k < C; ++k) {
+              const float2 v2 = *reinterpret_cast<const float2*>(vp + k * NPS);
+              const float4 w4 = *reinterpret_cast<const float4*>(wp + k * Cp);
+              acc[0][0] = fmaf(w4.x, v2.x, acc[0][0]); acc[0][1] = fmaf(w4.x, v2.y, acc[0][1]);
+              acc[1][0] = fmaf(w4.y, v2.x, acc[1][0]); acc[1][1] = fmaf(w4.y, v2.y, acc[1][1]);
+              acc[2][0] = fmaf(w4.z, v2.x, acc[2][0]); acc[2][1] = fmaf(w4.z, v2.y, acc[2][1]);
+              acc[3][0] = fmaf(w4.w, v2.x, acc[3][0]); acc[3][1] = fmaf(w4.w, v2.y, acc[3][1]);
+            }
+            const long long gs = tbase + (long long)p.Qz * s * T + 2 * tx;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int o = c0 + j;
-              if (o < C) {
-                float val = d8[j] + U[o * npad + m];
-                const long long gi = gs + o * chan_stride;
-                if (EPI == EPI_FWD) {
-                  val += bs[o];
-                  if (p.zsave) __stcs(p.zsave + gi, val);
-                  __stcs(p.out + gi, p.act_gelu ? gelu_f(val) : val);
-                } else {
-                  __stcs(p.out + gi, val);
+            for (int a = 0; a < 4; ++a) {
+              const int o = 4 * g + a;
+              if (o >= C) break;
+              const float2 u2 = *reinterpret_cast<const float2*>(U + o * NPS + p0);
+              float* out = p.out + gs + o * chan_stride;
+              float v0 = acc[a][0] + u2.x, v1 = acc[a][1] + u2.y;
+              if (EPI == EPI_FWD) {
+                v0 += bs[o];
+                v1 += bs[o];
+                if (p.zsave) {
+                  float* zo = p.zsave + gs + o * chan_stride;
+                  if (ok0) __stcs(zo, v0);
+                  if (ok1) __stcs(zo + 1, v1);
+                }
+                if (p.act_gelu) {
+                  v0 = gelu_f(v0);
+                  v1 = gelu_f(v1);
                 }
               }
+              if (ok0) __stcs(out, v0);
+              if (ok1) __stcs(out + 1, v1);
             }
           }
         }
-        if (BWD && h == 0 && 32 * q < C) {
-          // this tile's dW/db (TMEM rows o, columns i; i = C is db) -> fp32 smem
-          // accumulator, keeping the tensor-core accumulation depth to one tile
-          const int o = 32 * q + lane;
-          for (int c0 = 0; c0 <= C; c0 += 8) {
-            float d8[8];
-            tmem_ld8(dbase + MT * L.N1 + c0, d8);
-            if (o < C) {
+        if (EPI == EPI_BWD && dw_thread) {
+          const float* Dz = V;
+          const float* Vv = V + 2 * C * NPS;
+          for (int q = pgrp; q < NPS / 2; q += NPG) {
+            const int p0 = 2 * q;
+            float2 dz2[4], v2[4];
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (c0 + j <= C) DWA[o * L.N2 + c0 + j] += d8[j];
+            for (int a = 0; a < 4; ++a) {
+              const int o = 4 * og_w + a, i = 4 * ig_w + a;
+              dz2[a] = (o < C) ? *reinterpret_cast<const float2*>(Dz + o * NPS + p0) : make_float2(0.f, 0.f);
+              v2[a] = (i < C) ? *reinterpret_cast<const float2*>(Vv + i * NPS + p0) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              if (ig_w == 0) dbacc[a] += dz2[a].x + dz2[a].y;
+#pragma unroll
+              for (int c2 = 0; c2 < 4; ++c2) {
+                dwacc[a][c2] = fmaf(dz2[a].x, v2[c2].x, dwacc[a][c2]);
+                dwacc[a][c2] = fmaf(dz2[a].y, v2[c2].y, dwacc[a][c2]);
+              }
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&bars[2 + b]);   // empty[b]
       }
+      __syncthreads();
+      buf ^= 1;
     }
   }
-  __syncthreads();
-  if (BWD) {
+  cp_wait<0>();
+  if (EPI == EPI_BWD) {
+    // fixed-order CTA reduction of the per-thread partials into dWpart[blockIdx.x]
+    __syncthreads();
+    float* red = reinterpret_cast<float*>(smem_raw + L.v0);  // >= 20 * CT floats (host-checked)
+    const int stride = 20;
+    if (dw_thread) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+#pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) red[tid * stride + a * 4 + c2] = dwacc[a][c2];
+        red[tid * stride + 16 + a] = dbacc[a];
+      }
+    }
+    __syncthreads();
     float* outp = p.dWpart + (long long)blockIdx.x * (C * C + C);
-    for (int e = tid; e < C * C + C; e += CT) {
-      if (e < C * C) {
-        const int o = e / C, i = e - o * C;
-        outp[e] = DWA[o * L.N2 + i];
-      } else {
-        outp[e] = DWA[(e - C * C) * L.N2 + C];
-      }
+    for (int e = tid; e < C * C + C; e += nt) {
+      int o, i, slot;
+      if (e < C * C) { o = e / C; i = e - o * C; slot = (o % 4) * 4 + (i % 4); }
+      else { o = e - C * C; i = 0; slot = 16 + (o % 4); }
+      const int bk = (o / 4) * G + (i / 4);
+      float s = 0.f;
+      for (int g2 = 0; g2 < NPG; ++g2) s += red[(g2 * NB + bk) * stride + slot];
+      outp[e] = s;
     }
-  }
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tmem, L.tcols);
   }
 }
 
+// smem bytes for a given chunk width; the BWD reduction reuses both V buffers
 static size_t c_smem_for(int C, int Z, int T, int mz, int mt, int LZ, int TCH, int mode) {
-  return c_layout(C, Z, T, mz, mt, LZ, TCH, mode).total;
+  CLayout L = c_layout(C, Z, T, mz, mt, LZ, TCH, mode);
+  size_t t = L.total;
+  if (mode == EPI_BWD) {
+    const size_t need = size_t(CT) * 20 * sizeof(float);
+    const size_t have = L.total - L.v0;
+    if (need > have) t += need - have;
+  }
+  return t;
 }
 
 void pass_c_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* TCH, int* VW, size_t* smem) {
   const size_t budget = 227 * 1024;
-  // candidate chunks: T, then divisors of T that are multiples of 4, then any
-  // multiple of 4 (descending) -- the first that fits
+  // candidate chunks: T, then multiples of 4 (descending), then 2, 1
   int tch = T;
   size_t s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
-  for (int pass = 0; pass < 2 && s > budget && mode != EPI_U; ++pass) {
-    for (int cand = (T - 1) & ~3; cand >= 4; cand -= 4) {
-      if (pass == 0 && T % cand) continue;
-      tch = cand;
-      s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
-      if (s <= budget) break;
-    }
+  for (int cand = (T - 1) & ~3; s > budget && cand >= 4; cand -= 4) {
+    tch = cand;
+    s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
+  }
+  for (int cand : {2, 1}) {
+    if (s <= budget) break;
+    tch = cand;
+    s = c_smem_for(C, Z, T, mz, mt, LZ, tch, mode);
   }
   int vw = 1;
   if (T % 4 == 0 && tch % 4 == 0) vw = 4;
@@ -614,7 +398,7 @@ void pass_c_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* T
 
 template <int LZ, int LT>
 static cudaError_t launch_c(const PassCParams& p, int mode, int grid, size_t smem, cudaStream_t st) {
-  void (*k)(PassCParams) = mode == EPI_U ? pass_c_u_kernel<LZ, LT>
+  void (*k)(PassCParams) = mode == EPI_U ? pass_c_kernel<LZ, LT, EPI_U>
                          : mode == EPI_FWD ? pass_c_kernel<LZ, LT, EPI_FWD>
                                            : pass_c_kernel<LZ, LT, EPI_BWD>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
