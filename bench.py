@@ -139,13 +139,13 @@ def stage_bytes(prob, plan_info):
         "fwd.b_x_inv": mode + H,
         "fwd.b_y_inv": H + slab_kz,
         "fwd.pass_c": slab + 4 * n + 4 * n + 4 * n,         # slab, v, y, z_save
-        "bwd.pass_a": 8 * n + slab,                          # dy, z -> slab
+        "bwd.pass_a": 12 * n + slab,                         # dy, z -> slab, dz
         "bwd.b_y_fwd": slab_kz + H,
         "bwd.b_x_fwd": H + mode,
         "bwd.mix": 2 * Rb + 3 * mode,                        # R, dR, V^, G^, W'^
         "bwd.b_x_inv": mode + H,
         "bwd.b_y_inv": H + slab_kz,
-        "bwd.pass_c": slab + 12 * n + 4 * n,                 # slab, dy, z, v, dv
+        "bwd.pass_c": slab + 8 * n + 4 * n,                  # slab, dz, v -> dv
         "fwd.exchange_1": slab * (P - 1) / P, "fwd.exchange_2": slab * (P - 1) / P,
         "bwd.exchange_1": slab * (P - 1) / P, "bwd.exchange_2": slab * (P - 1) / P,
     }

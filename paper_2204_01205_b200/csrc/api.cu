@@ -100,7 +100,7 @@ struct fno_plan_s {
   // workspace (bytes offsets)
   void* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, total;
+  size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, o_dz, total;
   size_t n_slab_xy, n_slab_kz, n_h, n_mode;
   int max_grid_c = 0;
   int dir = 0;  // 0 forward call, 1 backward call (profiling labels)
@@ -348,6 +348,7 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   p->o_dwpart = take(size_t(p->max_grid_c) * dwlen * 4);
   p->o_dwloc = take(dwlen * 4);
   p->o_dwall = take(size_t(P) * dwlen * 4);
+  p->o_dz = take(size_t(p->B) * p->C * p->Xl * p->Yl * p->Z * p->T * 4);   // dz = dy * sigma'(z) (bwd)
   p->total = off;
   *out = p;
   return FNO_OK;
@@ -498,6 +499,7 @@ fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode
   a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->np_a[mode];
   a.C = p->C; a.Xl = int(p->Xl); a.Yl = int(p->Yl);
   a.use_tma = p->tma_a;
+  a.dz_out = wsp<float>(p, p->o_dz);
   a.slab = make_kzslab(p);
   FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a_m[mode], p->smem_a[mode], st), "pass A");
   return FNO_OK;
@@ -651,7 +653,7 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
   FNO_TRY(spectral_bwd_to_slab(p, dy, z_saved, mode, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
                                static_cast<float2*>(dR), accumulate, st));
   PassCParams c = make_c(p, EPI_BWD);
-  c.v = v; c.dy = dy; c.zs = z_saved; c.W = W; c.out = dv;
+  c.v = v; c.dy = p->act_gelu ? wsp<float>(p, p->o_dz) : dy; c.W = W; c.out = dv;   // dz formed by pass A
   c.dWpart = wsp<float>(p, p->o_dwpart);
   FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
   const int len = p->C * p->C + p->C;

@@ -122,9 +122,30 @@ __global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
       cp_wait<1>();
       __syncthreads();
     }
-    if (MODE == MODE_DZ_GELU) {  // dz = dy * gelu'(z_saved), in place
+    if (MODE == MODE_DZ_GELU) {  // dz = dy * gelu'(z_saved), in place; also kept for pass C
       const float* zs = stage + NP * ZT;
-      for (int i = tid; i < np * ZT; i += nt) stage[i] *= gelu_prime_f(zs[i]);
+      float* dzo = p.dz_out + plane0 * ZT;
+      if ((ZT & 3) == 0) {
+        float4* s4 = reinterpret_cast<float4*>(stage);
+        const float4* z4 = reinterpret_cast<const float4*>(zs);
+        float4* o4 = reinterpret_cast<float4*>(dzo);
+        for (int i = tid; i < np * ZT / 4; i += nt) {
+          float4 d = s4[i];
+          const float4 zz = z4[i];
+          d.x *= gelu_prime_f(zz.x);
+          d.y *= gelu_prime_f(zz.y);
+          d.z *= gelu_prime_f(zz.z);
+          d.w *= gelu_prime_f(zz.w);
+          s4[i] = d;
+          __stcs(o4 + i, d);
+        }
+      } else {
+        for (int i = tid; i < np * ZT; i += nt) {
+          const float d = stage[i] * gelu_prime_f(zs[i]);
+          stage[i] = d;
+          dzo[i] = d;
+        }
+      }
       fence_proxy_async();  // generic writes before the buffer is refilled by TMA
       __syncthreads();
     }

@@ -23,7 +23,7 @@ struct CLayout {
   size_t ws, bias, s, bb, u, v0, v1, twz, twt, dmap, total;
 };
 
-__host__ __device__ inline int c_num_arrays(int mode) { return mode == EPI_U ? 0 : (mode == EPI_FWD ? 1 : 3); }
+__host__ __device__ inline int c_num_arrays(int mode) { return mode == EPI_U ? 0 : (mode == EPI_FWD ? 1 : 2); }
 
 // tile rows have stride RS (even, and a multiple of 4 when TCH is) so point
 // pairs and 16-byte async copies stay aligned
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
   short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nk = L.nk, TP = L.TP, Cp = L.Cp, NPS = L.NPS, RS = L.RS;
-  constexpr int NA = (EPI == EPI_U) ? 0 : (EPI == EPI_FWD ? 1 : 3);
+  constexpr int NA = (EPI == EPI_U) ? 0 : (EPI == EPI_FWD ? 1 : 2);
   const long long ZT = (long long)Z * T;
   const long long chan_stride = (long long)p.Xl * p.Yl * ZT;
   const int G = (C + 3) / 4;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
       const int so = c * NPS + s * RS + vv * VW;
 #pragma unroll
       for (int a = 0; a < NA; ++a) {
-        const float* src = (EPI == EPI_FWD) ? p.v : (a == 0 ? p.dy : (a == 1 ? p.zs : p.v));
+        const float* src = (EPI == EPI_FWD) ? p.v : (a == 0 ? p.dy : p.v);   // bwd: dz (pass A), v
         float* d = dst + a * C * NPS + so;
         if (VW == 4) cp_async16(d, src + g);
         else if (VW == 2) cp_async8(d, src + g);
@@ -246,22 +246,16 @@ __global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
         float* V = reinterpret_cast<float*>(smem_raw + (buf ? L.v1 : L.v0));
         const bool ok0 = 2 * tx < tcw, ok1 = 2 * tx + 1 < tcw;
         if (EPI == EPI_BWD) {
-          // dz = dy * sigma'(z) in place; zero the invalid slots so dW sees exact zeros
-          for (int r = ty; ty < TY && r < C * LZ; r += TY) {
-            float* dzr = V + r * RS + 2 * tx;
-            const float* zr = V + C * NPS + r * RS + 2 * tx;
-            float* vr = V + 2 * C * NPS + r * RS + 2 * tx;
-            float2 d2 = *reinterpret_cast<float2*>(dzr);
-            const float2 z2 = *reinterpret_cast<const float2*>(zr);
-            if (p.act_gelu) {
-              d2.x *= gelu_prime_f(z2.x);
-              d2.y *= gelu_prime_f(z2.y);
+          // zero the invalid slots (ragged t chunk) so dW sees exact zeros
+          if (tcw < RS) {
+            for (int r = ty; ty < TY && r < C * LZ; r += TY) {
+              float* dzr = V + r * RS + 2 * tx;
+              float* vr = V + C * NPS + r * RS + 2 * tx;
+              if (!ok0) { dzr[0] = 0.f; vr[0] = 0.f; }
+              if (!ok1) { dzr[1] = 0.f; vr[1] = 0.f; }
             }
-            if (!ok0) { d2.x = 0.f; vr[0] = 0.f; }
-            if (!ok1) { d2.y = 0.f; vr[1] = 0.f; }
-            *reinterpret_cast<float2*>(dzr) = d2;
+            __syncthreads();
           }
-          __syncthreads();
         }
         // ---- phase 3: 1x1 channel linear + epilogue; rows (o-group, s) x pairs
         if (ty < TY) {
@@ -307,7 +301,7 @@ __global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
         }
         if (EPI == EPI_BWD && dw_thread) {
           const float* Dz = V;
-          const float* Vv = V + 2 * C * NPS;
+          const float* Vv = V + C * NPS;
           for (int q = pgrp; q < NPS / 2; q += NPG) {
             const int p0 = 2 * q;
             float2 dz2[4], v2[4];

@@ -31,7 +31,15 @@ while i < len(rows):
             body.append(rows[j]); j += 1
         # match function by instruction count
         base = int(body[0][0], 16)
-        best = max(funcs.items(), key=lambda kv: (len(kv[1]) == len(body), -abs(len(kv[1]) - len(body))))
+        mm = re.search(r"(\w+)<([^>]*)>", kname)
+        best = None
+        if mm:
+            targs = "".join("Li%sE" % a.split(")")[-1].strip() for a in mm.group(2).split(","))
+            key = mm.group(1) + "I" + targs
+            cands = [kv for kv in funcs.items() if key in kv[0]]
+            if cands: best = cands[0]
+        if best is None:
+            best = max(funcs.items(), key=lambda kv: (len(kv[1]) == len(body), -abs(len(kv[1]) - len(body))))
         lines = best[1]
         inst = collections.Counter(); samp = collections.Counter(); tot = 0; tots = 0
         for r in body:
