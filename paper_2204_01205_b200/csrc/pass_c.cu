@@ -334,24 +334,32 @@ __global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
                 }
               }
             }
+            // fixed-order transpose-reduction of the 32 dW partials over the 32
+            // lanes (31 shuffles instead of 160): at each level a lane keeps the
+            // half of its values selected by its lane bit and adds the partner's
+            // copy of that half; lane l ends with the total of value l = (a, c2)
             {
-              // fixed-order butterfly reduction over the 32 lanes, then accumulate
+              float* v = &acc[0][0];
 #pragma unroll
-              for (int a = 0; a < 4; ++a) {
+              for (int n = 16; n > 0; n >>= 1) {
+                const bool up = (lane & n) != 0;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) dsum[a] += __shfl_xor_sync(0xffffffffu, dsum[a], off);
-#pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2)
-#pragma unroll
-                  for (int off = 16; off > 0; off >>= 1) acc[a][c2] += __shfl_xor_sync(0xffffffffu, acc[a][c2], off);
+                for (int j = 0; j < n; ++j) {
+                  const float send = up ? v[j] : v[j + n];
+                  const float keep = up ? v[j + n] : v[j];
+                  v[j] = keep + __shfl_xor_sync(0xffffffffu, send, n);
+                }
               }
-              if (lane == 0) {
-                float* dst = DWS + bk * 36;
+              float* dst = DWS + bk * 36;
+              dst[lane] += v[0];
+              if (ig == 0) {
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
+                for (int a = 0; a < 4; ++a)
 #pragma unroll
-                  for (int c2 = 0; c2 < 8; ++c2) dst[a * 8 + c2] += acc[a][c2];
-                  if (ig == 0) dst[32 + a] += dsum[a];
+                  for (int off = 16; off > 0; off >>= 1) dsum[a] += __shfl_xor_sync(0xffffffffu, dsum[a], off);
+                if (lane == 0) {
+#pragma unroll
+                  for (int a = 0; a < 4; ++a) dst[32 + a] += dsum[a];
                 }
               }
             }
