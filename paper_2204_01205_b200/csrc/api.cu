@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -96,6 +97,7 @@ struct fno_plan_s {
   size_t smem_a[3] = {0, 0, 0}, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
   int np_a[3] = {1, 1, 1}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
+  int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -307,6 +309,19 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_U, &p->tch[0], &p->vw[0], &p->smem_c_u);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
+  {
+    const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
+    if (!(legacy && legacy[0] == '1')) {
+      int cp, tch, vw;
+      size_t sm;
+      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &vw, &sm)) {
+        p->c2cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->vw[EPI_FWD] = vw; p->smem_c_fwd = sm;
+      }
+      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm)) {
+        p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm;
+      }
+    }
+  }
   const size_t smem_max = 227 * 1024;
   if (p->smem_a[MODE_DZ_GELU] > smem_max || p->smem_c_bwd > smem_max) {
     char buf[200];
@@ -546,6 +561,11 @@ PassCParams make_c(fno_plan_t p, int mode) {
   return c;
 }
 
+cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c, int mode, int grid, size_t smem, cudaStream_t st) {
+  if (p->c2cp[mode] > 0) return launch_pass_c2(c, p->LZ, p->LT, p->c2cp[mode], mode, grid, smem, st);
+  return launch_pass_c(c, p->LZ, p->LT, mode, grid, smem, st);
+}
+
 fno_status check_ready(fno_plan_t p, const char* who) {
   if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": NULL plan");
   if (!p->ws) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": workspace not set (fno_plan_set_workspace)");
@@ -636,7 +656,7 @@ extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R,
   FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
   PassCParams c = make_c(p, EPI_FWD);
   c.v = v; c.W = W; c.bias = b; c.out = y; c.zsave = z_save;
-  FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
   return FNO_OK;
 }
 
@@ -655,7 +675,7 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
   PassCParams c = make_c(p, EPI_BWD);
   c.v = v; c.dy = p->act_gelu ? wsp<float>(p, p->o_dz) : dy; c.W = W; c.out = dv;   // dz formed by pass A
   c.dWpart = wsp<float>(p, p->o_dwpart);
-  FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
   const int len = p->C * p->C + p->C;
   if (p->P == 1) {
     FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, p->grid_c_bwd, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");

@@ -59,6 +59,7 @@ struct PassCParams {
   long long n_cols;     // B*Xl*Yl
   int B, C, Xl, Yl, Z, T, mz, mt, Qz, Qt;
   int TCH, VW;          // t-chunk of a tile, cp.async vector width (floats)
+  int use_tma;          // pass_c2: tile inputs by TMA tensor maps (T % 4 == 0)
   int act_gelu;         // 1: sigma = GELU, 0: identity
   float inv_n;          // 1 / (X Y Z T)
   KzSlab slab;

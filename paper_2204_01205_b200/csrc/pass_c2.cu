@@ -1,0 +1,91 @@
+// Host side of the channel-width-specialised pass C (kernel: pass_c2.cuh;
+// one translation unit per padded width CP so the instantiations compile in
+// parallel): tile configuration and the TMA tensor maps of the tile inputs.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "pass_c2.cuh"
+
+namespace fno {
+
+bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem) {
+  if (mode == EPI_U) return false;
+  const int CP = (C + 3) & ~3;
+  if (CP > 24) return false;
+  const size_t budget = 227 * 1024;
+  // t chunk: a multiple of 4 with LZ * TCH <= 256 (one 1x1 item per thread),
+  // at most T rounded up to 4; the largest that fits shared memory
+  int tmax = (T + 3) & ~3;
+  if (tmax * LZ > C2T) tmax = (C2T / LZ) & ~3;
+  if (tmax > 16 && T > 16) tmax = 16;
+  int tch = 0;
+  size_t s = 0;
+  for (int cand = tmax; cand >= 4; cand -= 4) {
+    s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode).total;
+    if (s <= budget) { tch = cand; break; }
+  }
+  if (!tch) return false;
+  int vw = 1;
+  if (T % 4 == 0) vw = 4;
+  else if (T % 2 == 0) vw = 2;
+  *CPo = CP;
+  *TCH = tch;
+  *VW = vw;
+  *smem = s;
+  return true;
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+// (T, Qz, LZ, Xl*Yl, B*C) view of an NCXYZT field; box [C][1][LZ][1][TCH]
+bool encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, int LZ) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return false;
+  const cuuint64_t dims[5] = {cuuint64_t(p.T), cuuint64_t(p.Qz), cuuint64_t(LZ), cuuint64_t(p.Xl) * p.Yl,
+                              cuuint64_t(p.B) * p.C};
+  const cuuint64_t ZT = cuuint64_t(p.Z) * p.T;
+  const cuuint64_t strides[4] = {cuuint64_t(p.T) * 4, cuuint64_t(p.Qz) * p.T * 4, ZT * 4,
+                                 cuuint64_t(p.Xl) * p.Yl * ZT * 4};
+  const cuuint32_t box[5] = {cuuint32_t(p.TCH), 1, cuuint32_t(LZ), 1, cuuint32_t(p.C)};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+cudaError_t launch_pass_c2(const PassCParams& p0, int LZ, int LT, int CP, int mode, int grid, size_t smem,
+                           cudaStream_t st) {
+  PassCParams p = p0;
+  C2Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  p.use_tma = 0;
+  if (p.T % 4 == 0 && p.TCH <= 256 && LZ <= 256 && p.C <= 256) {
+    const float* src0 = mode == EPI_FWD ? p.v : p.dy;
+    bool ok = encode_tile_map(&maps.m[0], src0, p, LZ);
+    if (ok && mode == EPI_BWD) ok = encode_tile_map(&maps.m[1], p.v, p, LZ);
+    p.use_tma = ok ? 1 : 0;
+  }
+  switch (CP) {
+    case 4: return launch_pass_c2_cp4(maps, p, LZ, LT, mode, grid, smem, st);
+    case 8: return launch_pass_c2_cp8(maps, p, LZ, LT, mode, grid, smem, st);
+    case 12: return launch_pass_c2_cp12(maps, p, LZ, LT, mode, grid, smem, st);
+    case 16: return launch_pass_c2_cp16(maps, p, LZ, LT, mode, grid, smem, st);
+    case 20: return launch_pass_c2_cp20(maps, p, LZ, LT, mode, grid, smem, st);
+    case 24: return launch_pass_c2_cp24(maps, p, LZ, LT, mode, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace fno
