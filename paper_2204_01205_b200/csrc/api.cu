@@ -98,6 +98,8 @@ struct fno_plan_s {
   int np_a[3] = {1, 1, 1}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
+  int a2 = 0, grid_a2 = 1;                     // warp-per-plane pass A (T <= 32)
+  size_t smem_a2 = 0;
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -310,6 +312,15 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
   {
+    // warp-per-plane pass A: opt-in (measured slower than the TMA-batched
+    // pass A at c2: 0.36 / 0.71 ms vs 0.27 / 0.60 ms per fwd / bwd launch)
+    const char* a2 = std::getenv("FNO_PASS_A2");
+    if (a2 && a2[0] == '1' && pass_a2_config(int(p->Z), int(p->T), p->mz, &p->smem_a2)) {
+      p->a2 = 1;
+      p->grid_a2 = pass_a2_grid((long long)p->B * p->C * p->Xl * p->Yl, int(p->T), p->num_sms);
+    }
+  }
+  {
     const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
     if (!(legacy && legacy[0] == '1')) {
       int cp, tch, vw;
@@ -516,7 +527,11 @@ fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode
   a.use_tma = p->tma_a;
   a.dz_out = wsp<float>(p, p->o_dz);
   a.slab = make_kzslab(p);
-  FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a_m[mode], p->smem_a[mode], st), "pass A");
+  if (p->a2) {
+    FNO_LAUNCH(p, ST_PASS_A, launch_pass_a2(a, p->LZ, p->LT, mode, p->grid_a2, p->smem_a2, st), "pass A");
+  } else {
+    FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a_m[mode], p->smem_a[mode], st), "pass A");
+  }
   return FNO_OK;
 }
 

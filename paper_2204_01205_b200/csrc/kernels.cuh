@@ -162,15 +162,27 @@ __device__ __forceinline__ int kmod_of(int j, int L, int n, int mneg) {
 // (|error| <= 1.5e-7 in erf; measured max |Phi error| 2.4e-7, |GELU error|
 // 3.1e-7, |GELU' error| 2.4e-7 over [-20, 20]), which shares exp(-z^2/2) with
 // the density: one MUFU.EX2 and one MUFU.RCP instead of erff + expf.
+__device__ __forceinline__ float rcp_approx_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx_ftz(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float normal_cdf_pdf(float z, float* pdf) {
   const float x = fabsf(z) * 0.70710678118654752440f;
-  const float t = __fdividef(1.0f, fmaf(0.3275911f, x, 1.0f));
-  float poly = fmaf(t, 1.061405429f, -1.453152027f);
-  poly = fmaf(t, poly, 1.421413741f);
-  poly = fmaf(t, poly, -0.284496736f);
-  poly = fmaf(t, poly, 0.254829592f);
-  const float e = __expf(-x * x);              // = exp(-z^2 / 2)
-  const float h = 0.5f * poly * t * e;         // Phi(-|z|)
+  const float t = rcp_approx_ftz(fmaf(0.3275911f, x, 1.0f));   // argument >= 1: no denormal path
+  // 0.5 * t * (a1 + t (a2 + t (a3 + t (a4 + t a5)))), the 1/2 folded into the coefficients
+  float poly = fmaf(t, 0.5307027145f, -0.7265760135f);
+  poly = fmaf(t, poly, 0.7107068705f);
+  poly = fmaf(t, poly, -0.142248368f);
+  poly = fmaf(t, poly, 0.127414796f);
+  poly *= t;
+  const float e = ex2_approx_ftz((z * z) * -0.72134752044448170368f);   // exp(-z^2 / 2)
+  const float h = poly * e;                     // Phi(-|z|)
   *pdf = 0.39894228040143267794f * e;
   return z >= 0.f ? 1.0f - h : h;
 }

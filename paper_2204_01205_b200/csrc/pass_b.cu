@@ -168,17 +168,28 @@ __global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
 // per-mode channel mixing (R_phi . F v on owned modes)
 // thread per retained mode m; complex fp32 accumulation
 // ---------------------------------------------------------------------------
+// Mixing is a weight stream at batch 1: each R element is read
+// once, coalesced across the mode-minor threads.  A thread owns one mode m and
+// a chunk of MCH outputs (fwd: o; bwd: i), so the grid has ceil(C / MCH) times
+// more warps in flight than a thread-per-mode kernel.
+constexpr int MCH = 4;
+
+// forward mixing: W^[b,o,m] = sum_i V^[b,i,m] R[i,o,m]
 template <int CMAX>
-__global__ void __launch_bounds__(128) mix_fwd_kernel(MixParams p) {
+__global__ void __launch_bounds__(256) mix_fwd_kernel(MixParams p) {
   const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= p.M) return;
   const int C = p.C;
+  const int o0 = blockIdx.y * MCH;
   for (int b = 0; b < p.B; ++b) {
     float2 vh[CMAX];
 #pragma unroll
     for (int i = 0; i < CMAX; ++i)
       if (i < C) vh[i] = __ldg(p.vhat + ((long long)b * C + i) * p.M + m);
-    for (int o = 0; o < C; ++o) {
+#pragma unroll 1
+    for (int oo = 0; oo < MCH; ++oo) {
+      const int o = o0 + oo;
+      if (o >= C) break;
       float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < CMAX; ++i)
@@ -191,37 +202,60 @@ __global__ void __launch_bounds__(128) mix_fwd_kernel(MixParams p) {
 // backward mixing: W'^[b,i,m] = sum_o G^[b,o,m] conj(R[i,o,m]);
 // dR[i,o,m] (+)= (c(kt)/N) sum_b conj(V^[b,i,m]) G^[b,o,m]
 template <int CMAX>
-__global__ void __launch_bounds__(128) mix_bwd_kernel(MixParams p) {
+__global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
   const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= p.M) return;
   const int C = p.C;
+  const int i0 = blockIdx.y * MCH;
   const int kt = int(m % p.mt);
   const float cw = (kt == 0 || ((p.T & 1) == 0 && 2 * kt == p.T)) ? 1.0f : 2.0f;
   const float scale = cw * p.inv_n;
+  float2 g[CMAX];
   for (int b = 0; b < p.B; ++b) {
-    float2 g[CMAX];
 #pragma unroll
     for (int o = 0; o < CMAX; ++o)
       if (o < C) g[o] = __ldg(p.ghat + ((long long)b * C + o) * p.M + m);
-    for (int i = 0; i < C; ++i) {
+#pragma unroll 1
+    for (int ii = 0; ii < MCH; ++ii) {
+      const int i = i0 + ii;
+      if (i >= C) break;
       float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
       for (int o = 0; o < CMAX; ++o)
-        if (o < C) acc = cfma_conj_a(__ldg(p.R + ((long long)i * C + o) * p.M + m), g[o], acc);
+        if (o < C) acc = cfma_conj_a(__ldcs(p.R + ((long long)i * C + o) * p.M + m), g[o], acc);
       p.what[((long long)b * C + i) * p.M + m] = acc;
     }
   }
-  if (p.dR != nullptr) {
-    for (int i = 0; i < C; ++i) {
-      for (int o = 0; o < C; ++o) {
-        float2 acc = make_float2(0.f, 0.f);
-        for (int b = 0; b < p.B; ++b)
-          acc = cfma_conj_a(__ldg(p.vhat + ((long long)b * C + i) * p.M + m), __ldg(p.ghat + ((long long)b * C + o) * p.M + m), acc);
-        float2* d = p.dR + ((long long)i * C + o) * p.M + m;
-        float2 val = cscale(acc, scale);
-        if (p.accumulate) val = cadd(*d, val);
-        *d = val;
+  if (p.dR == nullptr) return;
+  if (p.B == 1) {   // g still holds G^[0, :, m]
+#pragma unroll 1
+    for (int ii = 0; ii < MCH; ++ii) {
+      const int i = i0 + ii;
+      if (i >= C) break;
+      const float2 vs = cscale(cconj(__ldg(p.vhat + (long long)i * p.M + m)), scale);
+#pragma unroll
+      for (int o = 0; o < CMAX; ++o) {
+        if (o < C) {
+          float2* d = p.dR + ((long long)i * C + o) * p.M + m;
+          float2 val = cmul(vs, g[o]);
+          if (p.accumulate) val = cadd(*d, val);
+          __stcs(d, val);
+        }
       }
+    }
+    return;
+  }
+  for (int ii = 0; ii < MCH; ++ii) {
+    const int i = i0 + ii;
+    if (i >= C) break;
+    for (int o = 0; o < C; ++o) {
+      float2 acc = make_float2(0.f, 0.f);
+      for (int b = 0; b < p.B; ++b)
+        acc = cfma_conj_a(__ldg(p.vhat + ((long long)b * C + i) * p.M + m), __ldg(p.ghat + ((long long)b * C + o) * p.M + m), acc);
+      float2* d = p.dR + ((long long)i * C + o) * p.M + m;
+      float2 val = cscale(acc, scale);
+      if (p.accumulate) val = cadd(*d, val);
+      *d = val;
     }
   }
 }
@@ -287,17 +321,28 @@ cudaError_t launch_b_yinv(const PassBParams& p, int L, cudaStream_t st) {
 template <class K>
 static cudaError_t launch_mix(K k, const MixParams& p, cudaStream_t st) {
   if (p.M <= 0) return cudaSuccess;
-  k<<<unsigned((p.M + 127) / 128), 128, 0, st>>>(p);
+  const dim3 grid(unsigned((p.M + 255) / 256), unsigned((p.C + MCH - 1) / MCH));
+  k<<<grid, 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_mix_fwd(const MixParams& p, cudaStream_t st) {
+  if (p.C <= 4) return launch_mix(mix_fwd_kernel<4>, p, st);
   if (p.C <= 8) return launch_mix(mix_fwd_kernel<8>, p, st);
+  if (p.C <= 12) return launch_mix(mix_fwd_kernel<12>, p, st);
+  if (p.C <= 16) return launch_mix(mix_fwd_kernel<16>, p, st);
+  if (p.C <= 20) return launch_mix(mix_fwd_kernel<20>, p, st);
+  if (p.C <= 24) return launch_mix(mix_fwd_kernel<24>, p, st);
   if (p.C <= 32) return launch_mix(mix_fwd_kernel<32>, p, st);
   if (p.C <= 64) return launch_mix(mix_fwd_kernel<64>, p, st);
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st) {
+  if (p.C <= 4) return launch_mix(mix_bwd_kernel<4>, p, st);
   if (p.C <= 8) return launch_mix(mix_bwd_kernel<8>, p, st);
+  if (p.C <= 12) return launch_mix(mix_bwd_kernel<12>, p, st);
+  if (p.C <= 16) return launch_mix(mix_bwd_kernel<16>, p, st);
+  if (p.C <= 20) return launch_mix(mix_bwd_kernel<20>, p, st);
+  if (p.C <= 24) return launch_mix(mix_bwd_kernel<24>, p, st);
   if (p.C <= 32) return launch_mix(mix_bwd_kernel<32>, p, st);
   if (p.C <= 64) return launch_mix(mix_bwd_kernel<64>, p, st);
   return cudaErrorInvalidValue;
