@@ -3,6 +3,7 @@
 // parallel): tile configuration and the TMA tensor maps of the tile inputs.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -10,21 +11,28 @@
 
 namespace fno {
 
-bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem) {
+bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem,
+                    int* MMA) {
   if (mode == EPI_U) return false;
   const int CP = (C + 3) & ~3;
   if (CP > 24) return false;
+  // tensor-core 1x1 (tf32 + bf16 cross terms): opt-in, measured slower than the
+  // FFMA 1x1 at c2 (1.00 / 0.90 vs 0.75 / 0.81 ms per fwd / bwd launch)
+  const char* use_mma = std::getenv("FNO_PASS_C_MMA");
+  const bool mma_ok = CP >= 8 && (use_mma && use_mma[0] == '1');
   const size_t budget = 227 * 1024;
-  // t chunk: a multiple of 4 with LZ * TCH <= 256 (one 1x1 item per thread),
-  // at most T rounded up to 4; the largest that fits shared memory
+  // t chunk: a multiple of 4 with LZ * TCH <= 256 (at most one 1x1 item per
+  // thread), at most 16 and at most T rounded up to 4; the largest that fits
   int tmax = (T + 3) & ~3;
-  if (tmax * LZ > C2T) tmax = (C2T / LZ) & ~3;
+  if (tmax * LZ > 256) tmax = (256 / LZ) & ~3;
   if (tmax > 16 && T > 16) tmax = 16;
-  int tch = 0;
+  int tch = 0, mma = 0;
   size_t s = 0;
   for (int cand = tmax; cand >= 4; cand -= 4) {
-    s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode).total;
-    if (s <= budget) { tch = cand; break; }
+    const int m = (mma_ok && cand % 8 == 0) ? 1 : 0;
+    const int XR = m ? ((CP + 7) & ~7) : CP;
+    s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode, XR).total;
+    if (s <= budget) { tch = cand; mma = m; break; }
   }
   if (!tch) return false;
   int vw = 1;
@@ -34,6 +42,7 @@ bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   *TCH = tch;
   *VW = vw;
   *smem = s;
+  *MMA = mma;
   return true;
 }
 

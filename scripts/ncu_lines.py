@@ -34,7 +34,7 @@ while i < len(rows):
         mm = re.search(r"(\w+)<([^>]*)>", kname)
         best = None
         if mm:
-            targs = "".join("Li%sE" % a.split(")")[-1].strip() for a in mm.group(2).split(","))
+            targs = "".join(("Lb%sE" if "bool" in a else "Li%sE") % a.split(")")[-1].strip() for a in mm.group(2).split(","))
             key = mm.group(1) + "I" + targs
             cands = [kv for kv in funcs.items() if key in kv[0]]
             if cands: best = cands[0]
