@@ -98,7 +98,6 @@ struct fno_plan_s {
   int np_a[3] = {1, 1, 1}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
-  int c2mma[3] = {0, 0, 0};                    // pass_c2 1x1 on tensor cores
   int a2 = 0, grid_a2 = 1;                     // warp-per-plane pass A (T <= 32)
   size_t smem_a2 = 0;
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
@@ -324,13 +323,13 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   {
     const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
     if (!(legacy && legacy[0] == '1')) {
-      int cp, tch, vw, mma;
+      int cp, tch, vw;
       size_t sm;
-      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &vw, &sm, &mma)) {
-        p->c2cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->vw[EPI_FWD] = vw; p->smem_c_fwd = sm; p->c2mma[EPI_FWD] = mma;
+      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &vw, &sm)) {
+        p->c2cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->vw[EPI_FWD] = vw; p->smem_c_fwd = sm;
       }
-      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm, &mma)) {
-        p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm; p->c2mma[EPI_BWD] = mma;
+      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm)) {
+        p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm;
       }
     }
   }
@@ -567,7 +566,6 @@ PassCParams make_c(fno_plan_t p, int mode) {
   PassCParams c{};
   c.TCH = p->tch[mode];
   c.VW = p->vw[mode];
-  c.use_mma = p->c2mma[mode];
   {
     static const int ablate = [] { const char* e = std::getenv("FNO_ABLATE"); return e ? std::atoi(e) : 0; }();
     c.ablate = ablate;

@@ -11,28 +11,23 @@
 
 namespace fno {
 
-bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem,
-                    int* MMA) {
+bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem) {
   if (mode == EPI_U) return false;
   const int CP = (C + 3) & ~3;
-  if (CP > 24) return false;
-  // tensor-core 1x1 (tf32 + bf16 cross terms): opt-in, measured slower than the
-  // FFMA 1x1 at c2 (1.00 / 0.90 vs 0.75 / 0.81 ms per fwd / bwd launch)
-  const char* use_mma = std::getenv("FNO_PASS_C_MMA");
-  const bool mma_ok = CP >= 8 && (use_mma && use_mma[0] == '1');
-  const size_t budget = 227 * 1024;
-  // t chunk: a multiple of 4 with LZ * TCH <= 256 (at most one 1x1 item per
-  // thread), at most 16 and at most T rounded up to 4; the largest that fits
+  if (CP > 20) return false;
+  // t chunk: a multiple of 4 with LZ * TCH <= 128 (one 1x1 quad item per
+  // thread) and at most T rounded up to 4; prefer the largest that lets two
+  // CTAs share an SM (<= 113 KB each), else the largest that fits one
   int tmax = (T + 3) & ~3;
-  if (tmax * LZ > 256) tmax = (256 / LZ) & ~3;
-  if (tmax > 16 && T > 16) tmax = 16;
-  int tch = 0, mma = 0;
+  if (tmax * LZ > C2T) tmax = (C2T / LZ) & ~3;
+  int tch = 0;
   size_t s = 0;
-  for (int cand = tmax; cand >= 4; cand -= 4) {
-    const int m = (mma_ok && cand % 8 == 0) ? 1 : 0;
-    const int XR = m ? ((CP + 7) & ~7) : CP;
-    s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode, XR).total;
-    if (s <= budget) { tch = cand; mma = m; break; }
+  for (size_t budget : {size_t(113) * 1024, size_t(227) * 1024}) {
+    for (int cand = tmax; cand >= 4 && !tch; cand -= 4) {
+      s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode).total;
+      if (s <= budget) tch = cand;
+    }
+    if (tch) break;
   }
   if (!tch) return false;
   int vw = 1;
@@ -42,7 +37,6 @@ bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   *TCH = tch;
   *VW = vw;
   *smem = s;
-  *MMA = mma;
   return true;
 }
 
@@ -92,7 +86,6 @@ cudaError_t launch_pass_c2(const PassCParams& p0, int LZ, int LT, int CP, int mo
     case 12: return launch_pass_c2_cp12(maps, p, LZ, LT, mode, grid, smem, st);
     case 16: return launch_pass_c2_cp16(maps, p, LZ, LT, mode, grid, smem, st);
     case 20: return launch_pass_c2_cp20(maps, p, LZ, LT, mode, grid, smem, st);
-    case 24: return launch_pass_c2_cp24(maps, p, LZ, LT, mode, grid, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
