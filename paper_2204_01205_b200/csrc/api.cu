@@ -95,7 +95,7 @@ struct fno_plan_s {
   int num_sms = 148;
   int grid_c = 1, grid_c_bwd = 1;
   size_t smem_a[3] = {0, 0, 0}, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
-  int np_a[3] = {1, 1, 1}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
+  int np_a[3] = {1, 1, 1}, ns_a[3] = {2, 2, 2}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
   int a2 = 0, grid_a2 = 1;                     // warp-per-plane pass A (T <= 32)
@@ -307,7 +307,7 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   }
 
   // pass A batching (planes per TMA batch) per input mode
-  for (int m = 0; m < 3; ++m) pass_a_config(int(p->Z), int(p->T), p->mz, m, &p->np_a[m], &p->smem_a[m], &p->tma_a);
+  for (int m = 0; m < 3; ++m) pass_a_config(int(p->Z), int(p->T), p->mz, m, &p->np_a[m], &p->ns_a[m], &p->smem_a[m], &p->tma_a);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_U, &p->tch[0], &p->vw[0], &p->smem_c_u);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
@@ -522,7 +522,7 @@ fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode
   a.in0 = in0; a.in1 = in1;
   a.out = wsp<float2>(p, p->o_slab_xy);
   a.n_planes = (long long)p->B * p->C * p->Xl * p->Yl;
-  a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->np_a[mode];
+  a.Z = int(p->Z); a.T = int(p->T); a.mz = p->mz; a.mt = p->mt; a.Qz = p->Qz; a.Qt = p->Qt; a.NP = p->np_a[mode]; a.NS = p->ns_a[mode];
   a.C = p->C; a.Xl = int(p->Xl); a.Yl = int(p->Yl);
   a.use_tma = p->tma_a;
   a.dz_out = wsp<float>(p, p->o_dz);

@@ -40,6 +40,7 @@ struct PassAParams {
   float2* out;          // kz-ordered slab
   long long n_planes;   // B*C*Xl*Yl
   int Z, T, mz, mt, Qz, Qt, NP;
+  int NS;               // pass A stage buffers (1 or 2)
   int C, Xl, Yl;
   int use_tma;          // 1: TMA bulk copies of plane batches (Z*T % 4 == 0)
   float* dz_out;        // MODE_DZ_GELU: dz = dy * gelu'(z) is also written here (read by pass C)

@@ -27,7 +27,7 @@
 namespace fno {
 
 // planes per batch NP, dynamic shared memory and TMA eligibility for a pass-A mode
-void pass_a_config(int Z, int T, int mz, int mode, int* NP, size_t* smem, int* use_tma);
+void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* smem, int* use_tma);
 cudaError_t launch_pass_a(const PassAParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
 
 // warp-per-plane pass A (pass_a2.cu) for T <= 32: false if not applicable

@@ -22,21 +22,23 @@
 
 namespace fno {
 
-static constexpr int AT = 256;
+static constexpr int AT = 128;   // threads per CTA; several CTAs per SM overlap their phases
 
 struct ALayout {
   size_t stage[2], bb, twz, twt, dmap, bar, total;
   int NA;
 };
 
-__host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mode) {
+// NS stage buffers (2: the batch after next streams in while one is transformed;
+// 1: the next batch streams in during phase 2 only)
+__host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mode, int NS) {
   ALayout L{};
   L.NA = (mode == MODE_DZ_GELU) ? 2 : 1;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 127) & ~size_t(127); return o; };
   const size_t sb = size_t(L.NA) * NP * Z * T * sizeof(float);
   L.stage[0] = take(sb);
-  L.stage[1] = take(sb);
+  L.stage[1] = NS == 2 ? take(sb) : L.stage[0];
   L.bb = take(size_t(NP) * (mz + 1) * (T + 1) * sizeof(float2));
   L.twz = take(size_t(Z) * sizeof(float2));
   L.twt = take(size_t(T) * sizeof(float2));
@@ -47,14 +49,15 @@ __host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mo
 }
 
 template <int LZ, int LT, int MODE>
-__global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
+__global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(PassAParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
   const int ZT = Z * T;
   const int NP = p.NP;
   const int nk = mz + 1;        // kz' = 0..mz
   const int TP = T + 1;         // padded row of B
-  const ALayout L = a_layout(Z, T, mz, NP, MODE);
+  const int NS = p.NS;
+  const ALayout L = a_layout(Z, T, mz, NP, MODE, NS);
   constexpr int NA = (MODE == MODE_DZ_GELU) ? 2 : 1;
   float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
   float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
@@ -106,9 +109,9 @@ __global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
 
   long long kb = blockIdx.x;
   issue(kb, 0);
-  if (kb + gridDim.x < n_batches) issue(kb + gridDim.x, 1);
+  if (NS == 2 && kb + gridDim.x < n_batches) issue(kb + gridDim.x, 1);
   else if (!tma) cp_commit();
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase_bits = 0u;   // mbarrier parity of stage b in bit b
   int sb = 0;
   for (; kb < n_batches; kb += gridDim.x) {
     const long long plane0 = kb * NP;
@@ -116,10 +119,11 @@ __global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
     const int np = left < NP ? int(left) : NP;
     float* stage = reinterpret_cast<float*>(smem_raw + L.stage[sb]);
     if (tma) {
-      mbar_wait(&bar[sb], phase[sb]);
-      phase[sb] ^= 1u;
+      mbar_wait(&bar[sb], (phase_bits >> sb) & 1u);
+      phase_bits ^= 1u << sb;
     } else {
-      cp_wait<1>();
+      if (NS == 2) cp_wait<1>();
+      else cp_wait<0>();
       __syncthreads();
     }
     if (MODE == MODE_DZ_GELU) {  // dz = dy * gelu'(z_saved), in place; also kept for pass C
@@ -161,8 +165,9 @@ __global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
         if (j < nk) bo[j * TP] = acc[j];
     }
     __syncthreads();
-    // stage buffer drained: prefetch the batch after next into it
-    const long long kn = kb + 2LL * gridDim.x;
+    // stage buffer drained: prefetch the batch after next (NS = 2) or the
+    // next batch (NS = 1) into it
+    const long long kn = kb + (long long)NS * gridDim.x;
     if (kn < n_batches) issue(kn, sb);
     else if (!tma) cp_commit();
     // ---- phase 2: t-DFT of complex rows (pencils (plane, kz')) ------------
@@ -200,21 +205,29 @@ __global__ void __launch_bounds__(AT, 1) pass_a_kernel(PassAParams p) {
       }
     }
     __syncthreads();  // Bb reused by the next batch
-    sb ^= 1;
+    if (NS == 2) sb ^= 1;
   }
   if (!tma) cp_wait<0>();
 }
 
-void pass_a_config(int Z, int T, int mz, int mode, int* NP, size_t* smem, int* use_tma) {
-  const size_t budget = 200 * 1024;
+void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* smem, int* use_tma) {
+  // one z-pencil per thread in phase 1: NP = AT / T planes per batch; two
+  // stage buffers when three CTAs still fit an SM, else one
   int np = (AT + T - 1) / T;
   if (np < 1) np = 1;
-  ALayout L = a_layout(Z, T, mz, np, mode);
-  while (np > 1 && L.total > budget) {
+  const size_t per3 = 74 * 1024;
+  int ns = 2;
+  ALayout L = a_layout(Z, T, mz, np, mode, ns);
+  if (L.total > per3) {
+    ns = 1;
+    L = a_layout(Z, T, mz, np, mode, ns);
+  }
+  while (np > 1 && L.total > 200 * 1024) {
     --np;
-    L = a_layout(Z, T, mz, np, mode);
+    L = a_layout(Z, T, mz, np, mode, ns);
   }
   *NP = np;
+  *NS = ns;
   *smem = L.total;
   *use_tma = ((size_t(Z) * T) % 4 == 0) ? 1 : 0;
 }
