@@ -48,7 +48,9 @@ __host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mo
   return L;
 }
 
-template <int LZ, int LT, int MODE>
+// HALF: mz = LZ / 2 (nk = LZ / 2 + 1 at compile time: the unused outputs of
+// the z codelet are dead code)
+template <int LZ, int LT, int MODE, bool HALF>
 __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(PassAParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
@@ -158,11 +160,12 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
       const int pl = pid / T, t = pid - pl * T;
       const float* col = stage + pl * ZT + t;
       float2 acc[LZ];
-      trunc_fwd<LZ>(acc, p.Qz, twZ, [&](int z) { return make_float2(col[z * T], 0.0f); }, nk, 0);
+      constexpr int NKH = LZ / 2 + 1;
+      trunc_fwd<LZ>(acc, p.Qz, twZ, [&](int z) { return make_float2(col[z * T], 0.0f); }, HALF ? NKH : nk, 0);
       float2* bo = Bb + (pl * nk) * TP + t;
 #pragma unroll
       for (int j = 0; j < LZ; ++j)
-        if (j < nk) bo[j * TP] = acc[j];
+        if (j < (HALF ? NKH : nk)) bo[j * TP] = acc[j];
     }
     __syncthreads();
     // stage buffer drained: prefetch the batch after next (NS = 2) or the
@@ -234,9 +237,11 @@ void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* sme
 
 template <int LZ, int LT>
 static cudaError_t launch_a(const PassAParams& p, int mode, int grid, size_t smem, cudaStream_t st) {
-  void (*k)(PassAParams) = mode == MODE_V ? pass_a_kernel<LZ, LT, MODE_V>
-                         : mode == MODE_DZ_GELU ? pass_a_kernel<LZ, LT, MODE_DZ_GELU>
-                                                : pass_a_kernel<LZ, LT, MODE_DZ_NONE>;
+  const bool half = 2 * p.mz == LZ;
+  void (*k)(PassAParams) =
+      mode == MODE_V ? (half ? pass_a_kernel<LZ, LT, MODE_V, true> : pass_a_kernel<LZ, LT, MODE_V, false>)
+      : mode == MODE_DZ_GELU ? (half ? pass_a_kernel<LZ, LT, MODE_DZ_GELU, true> : pass_a_kernel<LZ, LT, MODE_DZ_GELU, false>)
+                             : (half ? pass_a_kernel<LZ, LT, MODE_DZ_NONE, true> : pass_a_kernel<LZ, LT, MODE_DZ_NONE, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   k<<<grid, AT, smem, st>>>(p);

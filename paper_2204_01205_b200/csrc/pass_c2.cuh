@@ -89,7 +89,9 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <int LZ, int LT, int CP, int EPI>
+// HALF: mz = LZ / 2 (nk = LZ / 2 + 1 at compile time: the zero z-spectrum
+// inputs of the inverse z codelet fold away)
+template <int LZ, int LT, int CP, int EPI, bool HALF>
 __global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
   static_assert(CP % 4 == 0, "CP must be a multiple of 4");
   constexpr int NA = (EPI == EPI_FWD) ? 1 : 2;
@@ -298,7 +300,8 @@ __global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__
         const int c = it / tcw, tt = it - c * tcw;
         float2 e[LZ];
 #pragma unroll
-        for (int i = 0; i < LZ; ++i) e[i] = (i < nk) ? Bb[(c * nk + i) * TP + t0 + tt] : make_float2(0.f, 0.f);
+        for (int i = 0; i < LZ; ++i)
+          e[i] = (i < (HALF ? LZ / 2 + 1 : nk)) ? Bb[(c * nk + i) * TP + t0 + tt] : make_float2(0.f, 0.f);
         float2 y[LZ];
         trunc_inv<LZ>(y, e, rz, twZ);
         float* uo = U + c * UPS + tt;
@@ -421,8 +424,10 @@ __global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__
 
 template <int LZ, int LT, int CP>
 cudaError_t launch_c2_cp(const C2Maps& maps, const PassCParams& p, int mode, int grid, size_t smem, cudaStream_t st) {
+  const bool half = 2 * p.mz == LZ;
   void (*k)(C2Maps, PassCParams) =
-      mode == EPI_FWD ? pass_c2_kernel<LZ, LT, CP, EPI_FWD> : pass_c2_kernel<LZ, LT, CP, EPI_BWD>;
+      mode == EPI_FWD ? (half ? pass_c2_kernel<LZ, LT, CP, EPI_FWD, true> : pass_c2_kernel<LZ, LT, CP, EPI_FWD, false>)
+                      : (half ? pass_c2_kernel<LZ, LT, CP, EPI_BWD, true> : pass_c2_kernel<LZ, LT, CP, EPI_BWD, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   k<<<grid, C2T, smem, st>>>(maps, p);
