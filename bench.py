@@ -32,7 +32,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "4D FNO layer grid-pts·ch/s fwd+bwd at 1/2/4/8 B200; % HBM/NVLink roofline"
 PGRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
-CONFIG_INDEX = 2            # BASELINE.json configs[1] (c2)
+CONFIG_INDEX = 2            # BASELINE.json configs[1] (c2); --config selects another
+STRONG = {"c3", "c5"}       # strong-scaled configs: the global grid is fixed (BASELINE.json)
+WORKLOADS = {
+    "c2": "c2: 4D Navier-Stokes-shaped DFNO training step (fwd+bwd), 64x64x64x32 per GPU, width 20, modes 8, "
+          "4 Fourier layers, batch 1 (BASELINE.json configs[1])",
+    "c3": "c3: CO2-multiphase-shaped DFNO training step (fwd+bwd), global 64x64x64x30, width 20, modes 12, "
+          "4 Fourier layers, batch 1, x/y-decomposed (strong scaling; BASELINE.json configs[2])",
+    "c4": "c4: weak-scaling 4D FNO, 64x128x128x32 per GPU, width 20, modes 12, 4 Fourier layers, fwd+bwd, batch 1 "
+          "(BASELINE.json configs[3])",
+    "c5": "c5: largest one-box instance, global 256x256x256x32, width 20, modes 16, 4 Fourier layers, fwd+bwd, "
+          "batch 1 (BASELINE.json configs[4])",
+}
 REF_WIDTH = 4               # oracle sample: channels per reference step
 
 
@@ -160,11 +171,13 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def load_traffic():
+def load_traffic(config):
+    """per-launch DRAM bytes of each stage from the committed `ncu --set full`
+    capture of this workload (profiles/ncu_traffic.json, keyed by config)"""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f)
+            return json.load(f).get(config, {})
     return {}
 
 
@@ -186,7 +199,8 @@ def run_ours(args, rank, world, local_rank):
     C, modes, L = cfg["width"], cfg["modes"], args.layers or cfg["layers"]
     B = args.batch
     px, py = PGRIDS[world]
-    grid = (lx * px, ly * py, Z, T)
+    strong = cfg["name"] in STRONG
+    grid = (lx, ly, Z, T) if strong else (lx * px, ly * py, Z, T)
     comm = fno.Comm.from_process_group() if world > 1 else None
     plan = fno.Plan(fno.Problem(grid=grid, width=C, modes=modes, batch=B, pgrid=(px, py)), comm, device=dev)
     kz_lo, kz_hi = plan.owned_modes()
@@ -301,7 +315,7 @@ def run_ours(args, rank, world, local_rank):
         tot_ms, cnt = kern[dom]
         avg_s = tot_ms / cnt / 1e3
         ach = sb[dom] / avg_s / 1e9
-        traffic = load_traffic().get(dom)
+        traffic = load_traffic(cfg["name"]).get(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic, "algorithmic_bytes": int(sb[dom]), "avg_launch_us": round(avg_s * 1e6, 2),
@@ -319,13 +333,13 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "grid-pts·ch/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded NS-shaped fields, random-init weights)",
-        "config": {"workload": "c2: 4D Navier-Stokes-shaped DFNO training step (fwd+bwd), 64x64x64x32 per GPU, "
-                               "width 20, modes 8, 4 Fourier layers, batch 1 (BASELINE.json configs[1])",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic (seeded {'CO2' if cfg['shape'] == 'co2' else 'NS'}-shaped fields, random-init weights)",
+        "config": {"workload": WORKLOADS[cfg["name"]],
                    "global_grid": list(grid), "pgrid": [px, py], "batch": B, "width": C, "modes": list(modes),
                    "layers": L, "parallelism": f"x/y domain decomposition {px}x{py}",
-                   "l2": "inputs larger than L2 (671 MB field per layer per GPU)"},
+                   "l2": f"inputs larger than L2 ({B * C * int(np.prod(local[2:])) * 4 / 1e6:.0f} MB field per "
+                         f"layer per GPU; L2 126 MB)"},
         "e2e": {"value": round(e2e_value, 1), "unit": "grid-pts·ch/s", "ms_per_step": round(e2e_ms, 4),
                 "h2d_bytes_per_step": int(h_v.numel() * 4 + h_dy.numel() * 4),
                 "d2h_bytes_per_step": int(h_out.numel() * 4)},
@@ -404,8 +418,8 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * wall / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded NS-shaped fields, random-init weights)",
-        "config": {"workload": "c2 per-GPU grid 64x64x64x32, modes 8; oracle sample: one DFNO block fwd+bwd at "
-                               f"width {REF_WIDTH} of 20 per step (bounded CPU sample)",
+        "config": {"workload": f"{cfg['name']} per-GPU grid {lx}x{ly}x{Z}x{T}, modes {modes[0]}; oracle sample: one "
+                               f"DFNO block fwd+bwd at width {REF_WIDTH} of 20 per step (bounded CPU sample)",
                    "grid": [lx, ly, Z, T], "width": REF_WIDTH, "modes": list(modes), "batch": 1},
         "cpu_baseline": cpu,
         "e2e": {"value": round(value, 1), "unit": "grid-pts·ch/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -422,7 +436,11 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c2",
+                    help="BASELINE.json workload (default c2 = configs[1]; c3 strong, c4 weak, c5 strong)")
     args = ap.parse_args()
+    global CONFIG_INDEX
+    CONFIG_INDEX = int(args.config[1])
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)

@@ -25,11 +25,13 @@ import collections
 def stage_of(name):
     m = re.match(r"(?:void )?(?:fno::)?(\w+?)(?:<(.*)>)?\(", name)
     base = m.group(1) if m else name.split("(")[0]
-    targs = [a.strip() for a in (m.group(2) or "").split(",")] if m else []
-    if base == "pass_a_kernel" and targs:
-        return "fwd.pass_a" if targs[-1] == "0" else "bwd.pass_a"
-    if base == "pass_c_kernel" and targs:
-        return {"0": "pass_c_u", "1": "fwd.pass_c", "2": "bwd.pass_c"}.get(targs[-1], base)
+    targs = [re.sub(r"\(\w+\)", "", a).strip() for a in (m.group(2) or "").split(",")] if m else []
+    if base in ("pass_a_kernel", "pass_a2_kernel") and len(targs) >= 3:       # <LZ, LT, MODE[, HALF]>
+        return "fwd.pass_a" if targs[2] == "0" else "bwd.pass_a"
+    if base == "pass_c_kernel" and len(targs) >= 3:                           # <LZ, LT, EPI>
+        return {"0": "pass_c_u", "1": "fwd.pass_c", "2": "bwd.pass_c"}.get(targs[2], base)
+    if base == "pass_c2_kernel" and len(targs) >= 4:                          # <LZ, LT, CP, EPI, HALF>
+        return {"1": "fwd.pass_c", "2": "bwd.pass_c"}.get(targs[3], base)
     if base == "mix_fwd_kernel":
         return "fwd.mix"
     if base == "mix_bwd_kernel":
@@ -111,6 +113,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic")
+    ap.add_argument("--config", default="c2", help="workload the capture ran (key of the traffic map)")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     md = []
@@ -126,10 +129,12 @@ def main():
                       f"{k['dram_pct_peak']:.1f} | {k['sm_pct_peak']:.1f} | {k['registers']} | "
                       f"{k['smem_per_block'] / 1024:.1f} | {k['grid']} x {k['block']} | {stalls} |")
         if a.traffic:
+            allt = json.load(open(a.traffic)) if os.path.exists(a.traffic) else {}
             tr = {}
             for k in ks:   # last capture of a stage wins (all launches of a stage move the same bytes)
                 tr[k["stage"]] = k["dram_bytes"]
-            json.dump(tr, open(a.traffic, "w"), indent=1, sort_keys=True)
+            allt[a.config] = tr
+            json.dump(allt, open(a.traffic, "w"), indent=1, sort_keys=True)
     if a.launches:
         fams = summarise_launches(a.launches)
         json.dump(fams, open(os.path.join(a.out, "ncu_launches_summary.json"), "w"), indent=1)
