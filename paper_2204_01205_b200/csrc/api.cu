@@ -98,6 +98,7 @@ struct fno_plan_s {
   int np_a[3] = {1, 1, 1}, ns_a[3] = {2, 2, 2}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
+  int c2nx[3] = {2, 2, 2};                     // pass_c2 X tile buffers
   int a2 = 0, grid_a2 = 1;                     // warp-per-plane pass A (T <= 32)
   size_t smem_a2 = 0;
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
@@ -323,13 +324,13 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   {
     const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
     if (!(legacy && legacy[0] == '1')) {
-      int cp, tch, vw;
+      int cp, tch, vw, nx;
       size_t sm;
-      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &vw, &sm)) {
-        p->c2cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->vw[EPI_FWD] = vw; p->smem_c_fwd = sm;
+      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &vw, &sm, &nx)) {
+        p->c2cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->vw[EPI_FWD] = vw; p->smem_c_fwd = sm; p->c2nx[EPI_FWD] = nx;
       }
-      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm)) {
-        p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm;
+      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm, &nx)) {
+        p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm; p->c2nx[EPI_BWD] = nx;
       }
     }
   }
@@ -566,6 +567,7 @@ PassCParams make_c(fno_plan_t p, int mode) {
   PassCParams c{};
   c.TCH = p->tch[mode];
   c.VW = p->vw[mode];
+  c.NX = p->c2nx[mode];
   {
     static const int ablate = [] { const char* e = std::getenv("FNO_ABLATE"); return e ? std::atoi(e) : 0; }();
     c.ablate = ablate;

@@ -42,7 +42,8 @@ cudaError_t launch_pass_c(const PassCParams& p, int LZ, int LT, int mode, int gr
 
 // channel-width-specialised pass C (pass_c2.cu) for the layer epilogues
 // (EPI_FWD / EPI_BWD) when C <= 20: false if the configuration is not covered
-bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CP, int* TCH, int* VW, size_t* smem);
+bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CP, int* TCH, int* VW, size_t* smem,
+                    int* NX);
 cudaError_t launch_pass_c2(const PassCParams& p, int LZ, int LT, int CP, int mode, int grid, size_t smem,
                            cudaStream_t st);
 

@@ -11,33 +11,37 @@
 
 namespace fno {
 
-bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem) {
+bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, int* VW, size_t* smem,
+                    int* NX) {
   if (mode == EPI_U) return false;
   const int CP = (C + 3) & ~3;
   if (CP > 20) return false;
   // t chunk: a multiple of 4 with LZ * TCH <= 128 (one 1x1 quad item per
-  // thread) and at most T rounded up to 4; prefer the largest that lets two
-  // CTAs share an SM (<= 113 KB each), else the largest that fits one
+  // thread) and at most T rounded up to 4.  Preference: three CTAs per SM with
+  // one X buffer (forward: the epilogue hides the next tile's load), two CTAs
+  // with two buffers, then the largest that fits one CTA
   int tmax = (T + 3) & ~3;
   if (tmax * LZ > C2T) tmax = (C2T / LZ) & ~3;
-  int tch = 0;
-  size_t s = 0;
-  for (size_t budget : {size_t(113) * 1024, size_t(227) * 1024}) {
-    for (int cand = tmax; cand >= 4 && !tch; cand -= 4) {
-      s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode).total;
-      if (s <= budget) tch = cand;
+  const char* nxe = std::getenv("FNO_PASS_C_NX");
+  const int force_nx = nxe ? std::atoi(nxe) : 0;
+  struct Opt { size_t budget; int nx; };
+  const Opt opts[] = {{75 * 1024, 1}, {113 * 1024, 2}, {227 * 1024, 2}, {227 * 1024, 1}};
+  for (const Opt& o : opts) {
+    if (force_nx && o.nx != force_nx) continue;
+    if (o.nx == 1 && mode != EPI_FWD && !force_nx) continue;   // bwd keeps two buffers
+    for (int cand = tmax; cand >= 4; cand -= 4) {
+      const size_t s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode, o.nx).total;
+      if (s <= o.budget) {
+        *CPo = CP;
+        *TCH = cand;
+        *VW = (T % 4 == 0) ? 4 : (T % 2 == 0) ? 2 : 1;
+        *smem = s;
+        *NX = o.nx;
+        return true;
+      }
     }
-    if (tch) break;
   }
-  if (!tch) return false;
-  int vw = 1;
-  if (T % 4 == 0) vw = 4;
-  else if (T % 2 == 0) vw = 2;
-  *CPo = CP;
-  *TCH = tch;
-  *VW = vw;
-  *smem = s;
-  return true;
+  return false;
 }
 
 namespace {

@@ -48,7 +48,10 @@ __host__ __device__ inline int c2_num_arrays(int mode) { return mode == EPI_FWD 
 
 // X tiles are dense [CP][LZ][TCH] (the TMA box layout); U rows are padded so
 // the phase-2 stores of lanes (c, t) fall on distinct banks
-__host__ __device__ inline C2Layout c2_layout(int CP, int C, int Z, int T, int mz, int mt, int LZ, int TCH, int mode) {
+// NX: X tile buffers (2: the next tile streams in during the whole tile; 1: it
+// streams in during the epilogue, leaving room for a third CTA per SM)
+__host__ __device__ inline C2Layout c2_layout(int CP, int C, int Z, int T, int mz, int mt, int LZ, int TCH, int mode,
+                                              int NX) {
   C2Layout L{};
   L.nk = mz + 1;
   L.TP = T + 1;
@@ -61,7 +64,7 @@ __host__ __device__ inline C2Layout c2_layout(int CP, int C, int Z, int T, int m
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 127) & ~size_t(127); return o; };
   L.x0 = take(size_t(NA) * CP * L.XPS * sizeof(float));
-  L.x1 = take(size_t(NA) * CP * L.XPS * sizeof(float));
+  L.x1 = NX == 2 ? take(size_t(NA) * CP * L.XPS * sizeof(float)) : L.x0;
   L.ws = take(size_t(CP) * L.WROW * sizeof(float));
   L.bias = take(size_t(CP) * sizeof(float));
   L.bb = take(size_t(C) * L.nk * L.TP * sizeof(float2));
@@ -92,14 +95,15 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
 // HALF: mz = LZ / 2 (nk = LZ / 2 + 1 at compile time: the zero z-spectrum
 // inputs of the inverse z codelet fold away)
 template <int LZ, int LT, int CP, int EPI, bool HALF>
-__global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
+__global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
   static_assert(CP % 4 == 0, "CP must be a multiple of 4");
   constexpr int NA = (EPI == EPI_FWD) ? 1 : 2;
   constexpr int Q4 = CP / 4;       // outputs per 1x1 item (output quarter)
   constexpr int DB = CP / 2;       // dW block: DB o-rows x DB i-columns per warp (2 x 2 warps)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt, TCH = p.TCH;
-  const C2Layout L = c2_layout(CP, C, Z, T, mz, mt, LZ, TCH, EPI);
+  const int NX = p.NX;
+  const C2Layout L = c2_layout(CP, C, Z, T, mz, mt, LZ, TCH, EPI, NX);
   float* Ws = reinterpret_cast<float*>(smem_raw + L.ws);
   float* bs = reinterpret_cast<float*>(smem_raw + L.bias);
   float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
@@ -275,15 +279,21 @@ __global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__
       const int rz = ti / nch, tc = ti - rz * nch;
       const int t0 = tc * TCH;
       const int tcw = min(TCH, T - t0);
-      if (ti + 1 < tpc) issue_tile(col, ti + 1, buf ^ 1);
-      else if (col_next < p.n_cols) issue_tile(col_next, 0, buf ^ 1);
+      if (NX == 2) {
+        if (ti + 1 < tpc) issue_tile(col, ti + 1, buf ^ 1);
+        else if (col_next < p.n_cols) issue_tile(col_next, 0, buf ^ 1);
+      }
       float* X = reinterpret_cast<float*>(smem_raw + (buf ? L.x1 : L.x0));
       if (tma) {
         mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);   // this tile's inputs (OOB t zero-filled)
         phase_bits ^= 1u << buf;
       } else {
-        cp_commit();
-        cp_wait<1>();
+        if (NX == 2) {
+          cp_commit();
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
         __syncthreads();
         if (EPI == EPI_BWD && tcw < TCH) {   // ragged t chunk: exact zeros for dW / db
           const int w = TCH - tcw;
@@ -355,7 +365,12 @@ __global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__
           for (int j = 0; j < Q4; ++j) acc[j] = f4fma(w[j], x4, acc[j]);
         }
       }
-      __syncthreads();   // U complete
+      __syncthreads();   // U complete; X no longer read by this tile
+      if (NX == 1) {       // single X buffer: the next tile streams in during the epilogue
+        if (ti + 1 < tpc) issue_tile(col, ti + 1, 0);
+        else if (col_next < p.n_cols) issue_tile(col_next, 0, 0);
+        if (!tma) cp_commit();
+      }
       // ---- epilogue: + u (+ b, GELU), stores -------------------------------
       if (item1 && tq1 < tcw && !(p.ablate & 4)) {
         const long long gs = cbase + rz * T + t0 + go1;
@@ -394,7 +409,7 @@ __global__ void __launch_bounds__(C2T, 2) pass_c2_kernel(const __grid_constant__
         }
       }
       __syncthreads();   // U and X[buf] free for reuse (and Bb after the last tile)
-      buf ^= 1;
+      if (NX == 2) buf ^= 1;
     }
   }
   cp_wait<0>();
