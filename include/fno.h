@@ -109,6 +109,19 @@ fno_status fno_plan_destroy(fno_plan_t plan);
 /* Bytes of device workspace the caller must provide (256-byte aligned). */
 fno_status fno_plan_workspace_size(fno_plan_t plan, size_t* bytes);
 fno_status fno_plan_set_workspace(fno_plan_t plan, void* dptr, size_t bytes);
+/* Collective (every rank of the plan's communicator calls it, after
+ * fno_plan_set_workspace): maps every rank's workspace into this process with
+ * CUDA IPC over NVLink, so that the pencil repartitions become
+ * direct peer stores -- pass A writes its retained-mode slab straight into the
+ * kz owners' receive buffers and the y-inverse writes straight into the x/y
+ * owners' receive buffers -- and each exchange reduces to a barrier (a one-int
+ * NCCL all-reduce).  Only the retained-mode slab crosses NVLink, as before.
+ * Stream-ordered on `stream` (synchronised once inside).  No-op when P == 1.
+ * The workspace must stay allocated for the plan's lifetime; the mappings are
+ * closed by fno_plan_destroy.  FNO_ERR_PLAN if the GPUs cannot access each
+ * other's memory, FNO_ERR_CUDA / FNO_ERR_NCCL on a failed mapping or
+ * all-gather (the plan then keeps using NCCL send/recv exchanges). */
+fno_status fno_plan_connect_peers(fno_plan_t plan, void* stream);
 /* Local x/y box of this rank in global coordinates: [lo, hi) per X, Y, Z, T. */
 fno_status fno_plan_local_box(fno_plan_t plan, int64_t lo[4], int64_t hi[4]);
 /* Retained-kz index block [kz_lo, kz_hi) whose weights this rank owns after the

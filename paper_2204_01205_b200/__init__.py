@@ -62,6 +62,7 @@ def lib() -> ctypes.CDLL:
             "fno_plan_destroy": [vp],
             "fno_plan_workspace_size": [vp, P(sz)],
             "fno_plan_set_workspace": [vp, vp, sz],
+            "fno_plan_connect_peers": [vp, vp],
             "fno_plan_local_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
             "fno_plan_owned_modes": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "fno_plan_vhat_elems": [vp, P(sz)],
@@ -187,7 +188,8 @@ class Comm:
 class Plan:
     """fno_plan_t plus its caller-owned workspace (a torch uint8 tensor)."""
 
-    def __init__(self, problem: Problem, comm: Optional[Comm] = None, device=None, allocate: bool = True):
+    def __init__(self, problem: Problem, comm: Optional[Comm] = None, device=None, allocate: bool = True,
+                 peer_exchange: Optional[bool] = None):
         self.problem = problem
         self.comm = comm
         h = ctypes.c_void_p()
@@ -201,6 +203,23 @@ class Plan:
             self.workspace = torch.empty(max(self.workspace_size(), 256), dtype=torch.uint8, device=dev)
             _check(lib().fno_plan_set_workspace(h, self.workspace.data_ptr(), self.workspace.numel()),
                    "fno_plan_set_workspace")
+            # direct NVLink stores for the pencil repartitions (collective; FNO_PEER_EXCHANGE=0 keeps
+            # the NCCL send/recv exchanges)
+            if peer_exchange is None:
+                peer_exchange = os.environ.get("FNO_PEER_EXCHANGE", "1") != "0"
+            if comm is not None and peer_exchange and self._nranks() > 1:
+                self.connect_peers()
+
+    def _nranks(self) -> int:
+        n, r = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().fno_comm_size(self.comm.handle, ctypes.byref(n), ctypes.byref(r)), "fno_comm_size")
+        return n.value
+
+    def connect_peers(self):
+        """Collective: map the peers' workspaces (fno_plan_connect_peers)."""
+        import torch
+        _check(lib().fno_plan_connect_peers(self.handle, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "fno_plan_connect_peers")
 
     def workspace_size(self) -> int:
         n = ctypes.c_size_t()

@@ -8,6 +8,7 @@
 //   fused with the DFNO block epilogue).
 // Only the retained-mode slab travels: truncation happens before the exchange
 // (reading Q9).
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -99,19 +100,22 @@ struct fno_plan_s {
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
   int c2nx[3] = {2, 2, 2};                     // pass_c2 X tile buffers
-  int a2 = 0, grid_a2 = 1;                     // warp-per-plane pass A (T <= 32)
-  size_t smem_a2 = 0;
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
   size_t ws_bytes = 0;
-  size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, o_dz, total;
+  size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, o_dz, o_bar, o_ipc, total;
+  // peer exchange (fno_plan_connect_peers): every rank's workspace mapped over NVLink
+  int peer = 0;
+  std::vector<char*> peer_ws;     // [P] workspace base of rank d in this process's address space
+  std::vector<void*> ipc_opened;  // mappings to close at destroy
   size_t n_slab_xy, n_slab_kz, n_h, n_mode;
   int max_grid_c = 0;
   int dir = 0;  // 0 forward call, 1 backward call (profiling labels)
   Prof prof;
   ~fno_plan_s() {
     for (cudaEvent_t e : prof.ev) cudaEventDestroy(e);
+    for (void* m : ipc_opened) cudaIpcCloseMemHandle(m);
   }
 };
 
@@ -313,15 +317,6 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
   {
-    // warp-per-plane pass A: opt-in (measured slower than the TMA-batched
-    // pass A at c2: 0.36 / 0.71 ms vs 0.27 / 0.60 ms per fwd / bwd launch)
-    const char* a2 = std::getenv("FNO_PASS_A2");
-    if (a2 && a2[0] == '1' && pass_a2_config(int(p->Z), int(p->T), p->mz, &p->smem_a2)) {
-      p->a2 = 1;
-      p->grid_a2 = pass_a2_grid((long long)p->B * p->C * p->Xl * p->Yl, int(p->T), p->num_sms);
-    }
-  }
-  {
     const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
     if (!(legacy && legacy[0] == '1')) {
       int cp, tch, vw, nx;
@@ -376,6 +371,8 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   p->o_dwloc = take(dwlen * 4);
   p->o_dwall = take(size_t(P) * dwlen * 4);
   p->o_dz = take(size_t(p->B) * p->C * p->Xl * p->Yl * p->Z * p->T * 4);   // dz = dy * sigma'(z) (bwd)
+  p->o_bar = take(256);                      // peer-exchange barrier word
+  p->o_ipc = take(size_t(P) * 256);          // peer-exchange handle all-gather
   p->total = off;
   *out = p;
   return FNO_OK;
@@ -398,6 +395,66 @@ extern "C" fno_status fno_plan_set_workspace(fno_plan_t p, void* dptr, size_t by
   if (reinterpret_cast<uintptr_t>(dptr) & 255) return fail(FNO_ERR_WORKSPACE, "fno_plan_set_workspace: workspace must be 256-byte aligned");
   p->ws = dptr;
   p->ws_bytes = bytes;
+  return FNO_OK;
+}
+
+// Collective: map every rank's workspace into this process (CUDA IPC over
+// NVLink) so pass A and the y-inverse store their exchange chunks straight
+// into the owners' receive buffers.  No-op for P == 1.
+extern "C" fno_status fno_plan_connect_peers(fno_plan_t p, void* stream) {
+  if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_connect_peers: NULL plan");
+  if (p->P == 1) return FNO_OK;
+  if (!p->ws) return fail(FNO_ERR_INVALID_STATE, "fno_plan_connect_peers: workspace not set");
+  if (!p->comm || !p->comm->nccl) return fail(FNO_ERR_INVALID_STATE, "fno_plan_connect_peers: communicator missing");
+  if (p->peer) return FNO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(FNO_ERR_CUDA, "fno_plan_connect_peers: cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t alloc = 0;
+  if (range(&base, &alloc, reinterpret_cast<CUdeviceptr>(p->ws)) != CUDA_SUCCESS)
+    return fail(FNO_ERR_CUDA, "fno_plan_connect_peers: workspace allocation range");
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    unsigned long long off;
+    int dev;
+  };
+  static_assert(sizeof(Rec) <= 256, "handle record");
+  Rec mine{};
+  FNO_CUDA(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)), "fno_plan_connect_peers: cudaIpcGetMemHandle");
+  mine.off = reinterpret_cast<CUdeviceptr>(p->ws) - base;
+  FNO_CUDA(cudaGetDevice(&mine.dev), "fno_plan_connect_peers: cudaGetDevice");
+  unsigned char* dbuf = static_cast<unsigned char*>(p->ws) + p->o_ipc;
+  FNO_CUDA(cudaMemcpyAsync(dbuf + size_t(p->rank) * 256, &mine, sizeof mine, cudaMemcpyHostToDevice, st), "ipc h2d");
+  FNO_NCCL(ncclAllGather(dbuf + size_t(p->rank) * 256, dbuf, 256, ncclUint8, p->comm->nccl, st), "ipc all-gather");
+  std::vector<unsigned char> all(size_t(p->P) * 256);
+  FNO_CUDA(cudaMemcpyAsync(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost, st), "ipc d2h");
+  FNO_CUDA(cudaStreamSynchronize(st), "fno_plan_connect_peers: sync");
+  std::vector<char*> bases(p->P, nullptr);
+  for (int d = 0; d < p->P; ++d) {
+    Rec r;
+    std::memcpy(&r, all.data() + size_t(d) * 256, sizeof r);
+    if (d == p->rank) {
+      bases[d] = static_cast<char*>(p->ws);
+      continue;
+    }
+    int can = 0;
+    FNO_CUDA(cudaDeviceCanAccessPeer(&can, mine.dev, r.dev), "cudaDeviceCanAccessPeer");
+    if (!can) return fail(FNO_ERR_PLAN, "fno_plan_connect_peers: no peer access between the ranks' GPUs");
+    void* m = nullptr;
+    FNO_CUDA(cudaIpcOpenMemHandle(&m, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    p->ipc_opened.push_back(m);
+    bases[d] = static_cast<char*>(m) + r.off;
+  }
+  p->peer_ws = bases;
+  p->peer = 1;
   return FNO_OK;
 }
 
@@ -468,6 +525,15 @@ KzSlab make_kzslab(fno_plan_t p) {
     s.off[d] = off;
     off += per * (p->kz_lo[d + 1] - p->kz_lo[d]);
   }
+  // pass A destinations: local send buffer, or this rank's block [src = rank] of
+  // owner d's kz-ordered receive buffer (chunks of per * nkz_d)
+  for (int d = 0; d < p->P; ++d) {
+    const long long nkz_d = p->kz_lo[d + 1] - p->kz_lo[d];
+    if (p->peer)
+      s.dst[d] = reinterpret_cast<float2*>(p->peer_ws[d] + p->o_slab_kz) + (long long)p->rank * per * nkz_d;
+    else if (p->ws)
+      s.dst[d] = wsp<float2>(p, p->o_slab_xy) + s.off[d];
+  }
   return s;
 }
 
@@ -481,8 +547,19 @@ PassBParams make_b(fno_plan_t p, const float2* in, float2* out, int Q) {
 }
 
 // exchange 1 (forward): kz-owner ordered send buffer -> x/y-source ordered receive buffer
+// peer exchange: the data already went over NVLink inside pass A / the
+// y-inverse; the exchange is a barrier (one-int NCCL all-reduce), after which
+// every rank's receive buffer is complete (writers fenced at system scope)
+fno_status peer_barrier(fno_plan_t p, int stage, const char* what, cudaStream_t st) {
+  StageScope sc(p, stage, st);
+  int* w = wsp<int>(p, p->o_bar);
+  FNO_NCCL(ncclAllReduce(w, w, 1, ncclInt, ncclSum, p->comm->nccl, st), what);
+  return FNO_OK;
+}
+
 fno_status exchange_fwd(fno_plan_t p, cudaStream_t st) {
   if (p->P == 1) return FNO_OK;
+  if (p->peer) return peer_barrier(p, ST_EX1, "exchange 1 (peer barrier)", st);
   const KzSlab s = make_kzslab(p);
   const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;  // complex per kz plane
   float2* send = wsp<float2>(p, p->o_slab_xy);
@@ -502,6 +579,7 @@ fno_status exchange_fwd(fno_plan_t p, cudaStream_t st) {
 // exchange 2 (adjoint): x/y-destination ordered -> kz-owner ordered
 fno_status exchange_bwd(fno_plan_t p, cudaStream_t st) {
   if (p->P == 1) return FNO_OK;
+  if (p->peer) return peer_barrier(p, ST_EX2, "exchange 2 (peer barrier)", st);
   const KzSlab s = make_kzslab(p);
   const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;
   float2* send = wsp<float2>(p, p->o_slab_kz);
@@ -528,11 +606,8 @@ fno_status run_pass_a(fno_plan_t p, const float* in0, const float* in1, int mode
   a.use_tma = p->tma_a;
   a.dz_out = wsp<float>(p, p->o_dz);
   a.slab = make_kzslab(p);
-  if (p->a2) {
-    FNO_LAUNCH(p, ST_PASS_A, launch_pass_a2(a, p->LZ, p->LT, mode, p->grid_a2, p->smem_a2, st), "pass A");
-  } else {
-    FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a_m[mode], p->smem_a[mode], st), "pass A");
-  }
+  a.peer = p->peer;
+  FNO_LAUNCH(p, ST_PASS_A, launch_pass_a(a, p->LZ, p->LT, mode, p->grid_a_m[mode], p->smem_a[mode], st), "pass A");
   return FNO_OK;
 }
 
@@ -552,7 +627,15 @@ fno_status run_b_inv(fno_plan_t p, const float2* what, cudaStream_t st) {
   float2* slab = wsp<float2>(p, p->o_slab_kz);
   float2* H = wsp<float2>(p, p->o_h);
   FNO_LAUNCH(p, ST_B_XI, launch_b_xinv(make_b(p, what, H, p->Qx), p->LX, st), "pass B x-inverse");
-  FNO_LAUNCH(p, ST_B_YI, launch_b_yinv(make_b(p, H, slab, p->Qy), p->LY, st), "pass B y-inverse");
+  PassBParams yb = make_b(p, H, slab, p->Qy);
+  // destinations of the y-inverse: local send buffer chunks [d], or this rank's
+  // block [owner = rank] of rank d's x/y-ordered receive buffer
+  const KzSlab ks = make_kzslab(p);
+  yb.P = p->P;
+  yb.peer = p->peer;
+  for (int d = 0; d < p->P; ++d)
+    yb.dst[d] = p->peer ? reinterpret_cast<float2*>(p->peer_ws[d] + p->o_slab_xy) + ks.off[p->rank] : slab + d * yb.chunk;
+  FNO_LAUNCH(p, ST_B_YI, launch_b_yinv(yb, p->LY, st), "pass B y-inverse");
   return FNO_OK;
 }
 

@@ -29,6 +29,9 @@ struct KzSlab {
   int P;
   int kz_lo[FNO_MAXP + 1];   // owner d holds retained kz [kz_lo[d], kz_lo[d+1])
   long long off[FNO_MAXP];   // complex-element offset of chunk d
+  float2* dst[FNO_MAXP];     // pass A: where owner d's chunk is written: the local send
+                             // buffer + off[d], or (peer exchange) this rank's block of
+                             // owner d's receive buffer, mapped over NVLink
 };
 
 enum { MODE_V = 0, MODE_DZ_GELU = 1, MODE_DZ_NONE = 2 };  // pass A input
@@ -44,6 +47,7 @@ struct PassAParams {
   int C, Xl, Yl;
   int use_tma;          // 1: TMA bulk copies of plane batches (Z*T % 4 == 0)
   float* dz_out;        // MODE_DZ_GELU: dz = dy * gelu'(z) is also written here (read by pass C)
+  int peer;             // 1: slab stores go straight to the peers (then a system fence per CTA)
   KzSlab slab;
 };
 
@@ -75,6 +79,10 @@ struct PassBParams {
   float2* out;
   int B, C, X, Y, Xl, Yl, py, nkz, mt, mx, my, Q;
   long long chunk;      // B*Xl*Yl*C*nkz*mt
+  int P;                // ranks
+  int peer;             // 1: y-inverse stores go straight to the peers (then a system fence per CTA)
+  float2* dst[FNO_MAXP];  // y-inverse: base of destination rank d's chunk (local send buffer
+                          // + d*chunk, or this rank's block of d's receive buffer over NVLink)
 };
 
 struct MixParams {

@@ -30,10 +30,6 @@ namespace fno {
 void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* smem, int* use_tma);
 cudaError_t launch_pass_a(const PassAParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
 
-// warp-per-plane pass A (pass_a2.cu) for T <= 32: false if not applicable
-bool pass_a2_config(int Z, int T, int mz, size_t* smem);
-int pass_a2_grid(long long n_planes, int T, int num_sms);
-cudaError_t launch_pass_a2(const PassAParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
 
 // chooses the t-chunk TCH (largest that fits shared memory), the cp.async
 // vector width VW and the dynamic shared memory size for a pass-C mode

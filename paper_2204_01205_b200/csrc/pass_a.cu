@@ -25,7 +25,7 @@ namespace fno {
 static constexpr int AT = 128;   // threads per CTA; several CTAs per SM overlap their phases
 
 struct ALayout {
-  size_t stage[2], bb, twz, twt, dmap, bar, total;
+  size_t stage[2], bb, twz, twt, dmap, jbase, jnk, bar, total;
   int NA;
 };
 
@@ -43,6 +43,8 @@ __host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mo
   L.twz = take(size_t(Z) * sizeof(float2));
   L.twt = take(size_t(T) * sizeof(float2));
   L.dmap = take(size_t(2 * mz) * sizeof(short2));
+  L.jbase = take(size_t(2 * mz) * sizeof(float2*));
+  L.jnk = take(size_t(2 * mz) * sizeof(int));
   L.bar = take(2 * sizeof(uint64_t));
   L.total = off;
   return L;
@@ -65,6 +67,8 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
   float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
   float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
   short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
+  float2** jbase = reinterpret_cast<float2**>(smem_raw + L.jbase);   // retained jz -> owner chunk + jl*mt
+  int* jnk = reinterpret_cast<int*>(smem_raw + L.jnk);               // retained jz -> owner's nkz
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
   const int tid = threadIdx.x, nt = blockDim.x;
   const long long n_batches = (p.n_planes + NP - 1) / NP;
@@ -76,6 +80,8 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
     int d = 0;
     while (j >= p.slab.kz_lo[d + 1]) ++d;
     dmap[j] = make_short2(short(d), short(j - p.slab.kz_lo[d]));
+    jbase[j] = p.slab.dst[d] + (long long)(j - p.slab.kz_lo[d]) * mt;
+    jnk[j] = p.slab.kz_lo[d + 1] - p.slab.kz_lo[d];
   }
   const bool tma = p.use_tma != 0;
   if (tid == 0 && tma) {
@@ -189,17 +195,14 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
       const int b = int(r1 / p.C);
       const long long pt = ((long long)(b * p.Xl + xl) * p.Yl + yl) * p.C + c;  // point-channel index in chunk
       if (kzp < mz) {  // kz = +kz' -> retained index jz = kz'
-        const short2 dm = dmap[kzp];
-        const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
-        float2* o = p.out + p.slab.off[dm.x] + (pt * nkz + dm.y) * mt;
+        float2* o = jbase[kzp] + pt * jnk[kzp] * mt;
 #pragma unroll
         for (int i = 0; i < LT; ++i)
           if (i < mt) o[i] = acc[i];
       }
       if (kzp >= 1) {  // kz = -kz' -> retained index jz = 2mz - kz'
-        const short2 dm = dmap[2 * mz - kzp];
-        const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
-        float2* o = p.out + p.slab.off[dm.x] + (pt * nkz + dm.y) * mt;
+        const int jz = 2 * mz - kzp;
+        float2* o = jbase[jz] + pt * jnk[jz] * mt;
 #pragma unroll
         for (int i = 0; i < LT; ++i) {
           const int kt = (LT - i) % LT;             // residue i holds frequency -kt
@@ -211,6 +214,10 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
     if (NS == 2) sb ^= 1;
   }
   if (!tma) cp_wait<0>();
+  if (p.peer) {   // slab stores went to peers over NVLink: publish them before the exchange barrier
+    __syncthreads();
+    if (tid == 0) __threadfence_system();
+  }
 }
 
 void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* smem, int* use_tma) {

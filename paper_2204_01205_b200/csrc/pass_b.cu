@@ -124,43 +124,60 @@ __global__ void __launch_bounds__(BT) b_xinv_kernel(PassBParams p) {
 }
 
 // y inverse: H' -> slab (x/y-destination ordered).  pencil = (b, kzl, o, x, kt)
+// Destination rank (sx, y / Yl) gets its chunk through dst[]: the local send
+// buffer for the NCCL exchange, or (peer exchange) its own receive buffer,
+// written over NVLink so exchange 2 needs no data movement of its own.
 template <int L>
 __global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* tw = reinterpret_cast<float2*>(smem_raw);
-  long long* ypart = reinterpret_cast<long long*>(tw + p.Y);
+  float2** dtab = reinterpret_cast<float2**>(smem_raw);                       // [P]
+  float2* tw = reinterpret_cast<float2*>(smem_raw + FNO_MAXP * sizeof(float2*));
+  long long* ypart = reinterpret_cast<long long*>(tw + p.Y);                  // (y % Yl) * cm
+  int* ydst = reinterpret_cast<int*>(ypart + p.Y);                            // y / Yl
   const int cm = p.C * p.nkz * p.mt;
-  for (int y = threadIdx.x; y < p.Y; y += blockDim.x) ypart[y] = (long long)(y / p.Yl) * p.chunk + (long long)(y % p.Yl) * cm;
+  for (int y = threadIdx.x; y < p.Y; y += blockDim.x) {
+    ypart[y] = (long long)(y % p.Yl) * cm;
+    ydst[y] = y / p.Yl;
+  }
+  for (int d = threadIdx.x; d < p.P; d += blockDim.x) dtab[d] = p.dst[d];
   fill_combine_table(tw, L, p.Q, p.Y, p.my, +1, threadIdx.x, blockDim.x);
   __syncthreads();
   const int my2 = 2 * p.my;
   const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
   const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (pid >= total) return;
-  const int kt = int(pid % p.mt);
-  long long r = pid / p.mt;
-  const int x = int(r % p.X);
-  r /= p.X;
-  const int oc = int(r % p.C);
-  r /= p.C;
-  const int kzl = int(r % p.nkz);
-  const int b = int(r / p.nkz);
-  const float2* __restrict__ in = p.in + (((long long)(b * p.nkz + kzl) * p.C + oc) * p.X + x) * my2 * p.mt + kt;
-  float2 e[L];
+  if (pid < total) {
+    const int kt = int(pid % p.mt);
+    long long r = pid / p.mt;
+    const int x = int(r % p.X);
+    r /= p.X;
+    const int oc = int(r % p.C);
+    r /= p.C;
+    const int kzl = int(r % p.nkz);
+    const int b = int(r / p.nkz);
+    const float2* __restrict__ in = p.in + (((long long)(b * p.nkz + kzl) * p.C + oc) * p.X + x) * my2 * p.mt + kt;
+    float2 e[L];
 #pragma unroll
-  for (int j = 0; j < L; ++j) {
-    if (j < p.my) e[j] = __ldg(in + (long long)j * p.mt);
-    else if (j >= L - p.my) e[j] = __ldg(in + (long long)(j - L + my2) * p.mt);
-    else e[j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < L; ++j) {
+      if (j < p.my) e[j] = __ldg(in + (long long)j * p.mt);
+      else if (j >= L - p.my) e[j] = __ldg(in + (long long)(j - L + my2) * p.mt);
+      else e[j] = make_float2(0.f, 0.f);
+    }
+    const int sx = x / p.Xl, xl = x - sx * p.Xl;
+    const long long o = ((long long)b * p.Xl + xl) * p.Yl * cm + (long long)(oc * p.nkz + kzl) * p.mt + kt;
+    float2* const* drow = dtab + sx * p.py;
+    for (int rc = 0; rc < p.Q; ++rc) {
+      float2 y[L];
+      trunc_inv<L>(y, e, rc, tw);
+#pragma unroll
+      for (int s = 0; s < L; ++s) {
+        const int yy = rc + p.Q * s;
+        drow[ydst[yy]][o + ypart[yy]] = y[s];
+      }
+    }
   }
-  const int sx = x / p.Xl, xl = x - sx * p.Xl;
-  float2* o = p.out + (long long)sx * p.py * p.chunk + ((long long)b * p.Xl + xl) * p.Yl * cm +
-              (long long)(oc * p.nkz + kzl) * p.mt + kt;
-  for (int rc = 0; rc < p.Q; ++rc) {
-    float2 y[L];
-    trunc_inv<L>(y, e, rc, tw);
-#pragma unroll
-    for (int s = 0; s < L; ++s) o[ypart[rc + p.Q * s]] = y[s];
+  if (p.peer) {   // stores went to peers over NVLink: publish them before the exchange barrier
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
   }
 }
 
@@ -311,7 +328,7 @@ cudaError_t launch_b_xinv(const PassBParams& p, int L, cudaStream_t st) {
 }
 cudaError_t launch_b_yinv(const PassBParams& p, int L, cudaStream_t st) {
   const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
-  const size_t smem = size_t(p.Y) * (sizeof(float2) + sizeof(long long));
+  const size_t smem = FNO_MAXP * sizeof(float2*) + size_t(p.Y) * (sizeof(float2) + sizeof(long long) + sizeof(int));
 #define FNO_CASE(l) if (L == l) return launch_pencils(b_yinv_kernel<l>, p, total, smem, st);
   FNO_B_SIZES(FNO_CASE)
 #undef FNO_CASE

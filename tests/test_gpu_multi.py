@@ -27,8 +27,10 @@ CASES = [((2, 1), [16, 16, 16, 8], 4, [4, 4, 4, 4], 1),
          ((4, 1), [16, 8, 16, 8], 2, [2, 2, 1, 4], 1)]    # 2mz = 2 < P: ranks with no modes
 
 
+# exchange transport: direct NVLink peer stores (default) or NCCL send/recv
+@pytest.mark.parametrize("peer", ["1", "0"], ids=["peer", "nccl"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"pg{c[0][0]}x{c[0][1]}_" + "x".join(map(str, c[1])))
-def test_decomposed_matches_single_and_oracle(case, tmp_path):
+def test_decomposed_matches_single_and_oracle(case, peer, tmp_path):
     pg, grid, C, modes, B = case
     n = pg[0] * pg[1]
     if _ngpu() < n:
@@ -40,7 +42,8 @@ def test_decomposed_matches_single_and_oracle(case, tmp_path):
            "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(ROOT, "tests", "mp_parity.py"),
            "--pgrid", str(pg[0]), str(pg[1]), "--grid", *map(str, grid), "--width", str(C),
            "--modes", *map(str, modes), "--batch", str(B), "--out", str(out)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, FNO_PEER_EXCHANGE=peer)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(out.read_text())
     for k, v in res.items():
