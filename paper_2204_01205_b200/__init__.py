@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfno.so")
+LIB_PATH = os.environ.get("FNO_LIB") or os.path.join(_PKG, "lib", "libfno.so")   # FNO_LIB: A/B builds
 
 FNO_ACT_GELU = 0
 FNO_ACT_NONE = 1

@@ -100,6 +100,7 @@ struct fno_plan_s {
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
   int c2nx[3] = {2, 2, 2};                     // pass_c2 X tile buffers
+  int c3cp[3] = {0, 0, 0};                     // > 0: tensor-core pass_c3 kernel with that padded width
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -326,6 +327,9 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
       }
       if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm, &nx)) {
         p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm; p->c2nx[EPI_BWD] = nx;
+      }
+      if (pass_c3_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &sm)) {
+        p->c3cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->smem_c_fwd = sm;
       }
     }
   }
@@ -666,6 +670,7 @@ PassCParams make_c(fno_plan_t p, int mode) {
 }
 
 cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c, int mode, int grid, size_t smem, cudaStream_t st) {
+  if (p->c3cp[mode] > 0) return launch_pass_c3(c, p->LZ, p->LT, p->c3cp[mode], grid, smem, st);
   if (p->c2cp[mode] > 0) return launch_pass_c2(c, p->LZ, p->LT, p->c2cp[mode], mode, grid, smem, st);
   return launch_pass_c(c, p->LZ, p->LT, mode, grid, smem, st);
 }

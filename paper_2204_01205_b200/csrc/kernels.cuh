@@ -139,18 +139,20 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned phase) {
   unsigned ok;
   asm volatile(
-      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n selp.u32 %0, 1, 0, P;\n}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(10000000u)
       : "memory");
   return ok != 0;
 }
 // bounded wait: a barrier that never completes (a malformed async copy or MMA)
-// traps the kernel instead of hanging the GPU
+// traps the kernel instead of hanging the GPU.  Each try_wait may suspend the
+// warp in hardware (time hint 10 ms) until the phase completes, so waiting
+// warps do not spin on the issue slots the working warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  unsigned long long spins = 0;
+  unsigned spins = 0;
   while (!mbar_try_wait(bar, phase)) {
-    if (++spins > (1ull << 26)) __trap();
+    if (++spins > (1u << 22)) __trap();
   }
 }
 
@@ -197,10 +199,20 @@ __device__ __forceinline__ float normal_cdf_pdf(float z, float* pdf) {
   *pdf = 0.39894228040143267794f * e;
   return z >= 0.f ? 1.0f - h : h;
 }
-// sigma = GELU(z) = z Phi(z) (exact-erf form, reading Q6) and its derivative
+// sigma = GELU(z) = z Phi(z) (exact-erf form, reading Q6) and its derivative.
+// Forward: Phi(z) = 1 / (1 + 2^(z P(min(z^2, 30.25)))) with a degree-6 P fitted
+// by scripts/fit_gelu.py (max |GELU error| 8.7e-7 in fp32 over [-10, 10],
+// relative 6.5e-7 where |GELU| > 0.05 -- as accurate as the A&S form, in 12
+// instructions instead of 17: one EX2, one RCP, no select).
 __device__ __forceinline__ float gelu_f(float z) {
-  float pdf;
-  return z * normal_cdf_pdf(z, &pdf);
+  const float u = fminf(z * z, 30.25f);
+  float q = fmaf(u, -4.677764398053341e-09f, 3.6614977716453723e-07f);
+  q = fmaf(u, q, -1.1269662536506075e-05f);
+  q = fmaf(u, q, 0.00015897156845312566f);
+  q = fmaf(u, q, 9.451490041101351e-05f);
+  q = fmaf(u, q, -0.10483447462320328f);
+  q = fmaf(u, q, -2.3022098541259766f);
+  return z * rcp_approx_ftz(1.0f + ex2_approx_ftz(z * q));
 }
 __device__ __forceinline__ float gelu_prime_f(float z) {
   float pdf;

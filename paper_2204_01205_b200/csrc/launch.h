@@ -43,6 +43,11 @@ bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
 cudaError_t launch_pass_c2(const PassCParams& p, int LZ, int LT, int CP, int mode, int grid, size_t smem,
                            cudaStream_t st);
 
+// tensor-core pass C (pass_c3.cu): layer forward with the 1x1 + bias on
+// tcgen05 (3xTF32, TMEM accumulator); false if the configuration is not covered
+bool pass_c3_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CP, int* TCH, size_t* smem);
+cudaError_t launch_pass_c3(const PassCParams& p, int LZ, int LT, int CP, int grid, size_t smem, cudaStream_t st);
+
 // pass B: y forward (slab -> H), x forward (H -> V^), x inverse (W^ -> H'),
 // y inverse (H' -> slab)
 cudaError_t launch_b_yfwd(const PassBParams& p, int L, cudaStream_t st);

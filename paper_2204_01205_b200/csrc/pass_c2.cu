@@ -47,9 +47,10 @@ bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
+}  // namespace
 
 // (T, Qz, LZ, Xl*Yl, B*C) view of an NCXYZT field; box [C][1][LZ][1][TCH]
-bool encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, int LZ) {
+bool c2_encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, int LZ) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -70,7 +71,6 @@ bool encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, in
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
-}  // namespace
 
 cudaError_t launch_pass_c2(const PassCParams& p0, int LZ, int LT, int CP, int mode, int grid, size_t smem,
                            cudaStream_t st) {
@@ -80,8 +80,8 @@ cudaError_t launch_pass_c2(const PassCParams& p0, int LZ, int LT, int CP, int mo
   p.use_tma = 0;
   if (p.T % 4 == 0 && p.TCH <= 256 && LZ <= 256 && p.C <= 256) {
     const float* src0 = mode == EPI_FWD ? p.v : p.dy;
-    bool ok = encode_tile_map(&maps.m[0], src0, p, LZ);
-    if (ok && mode == EPI_BWD) ok = encode_tile_map(&maps.m[1], p.v, p, LZ);
+    bool ok = c2_encode_tile_map(&maps.m[0], src0, p, LZ);
+    if (ok && mode == EPI_BWD) ok = c2_encode_tile_map(&maps.m[1], p.v, p, LZ);
     p.use_tma = ok ? 1 : 0;
   }
   switch (CP) {

@@ -449,6 +449,10 @@ cudaError_t launch_c2_cp(const C2Maps& maps, const PassCParams& p, int mode, int
   return cudaGetLastError();
 }
 
+// TMA tensor map of a tile input: (T, Qz, LZ, Xl*Yl, B*C) view of an NCXYZT
+// field, box [C][1][LZ][1][p.TCH] (pass_c2.cu)
+bool c2_encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, int LZ);
+
 // per-width entry points (one translation unit per CP: pass_c2_cp<CP>.cu)
 cudaError_t launch_pass_c2_cp4(const C2Maps& maps, const PassCParams& p, int LZ, int LT, int mode, int grid, size_t smem,
                                cudaStream_t st);
