@@ -16,8 +16,10 @@ Parity status per function:
   spectral.forward_modes / inverse_modes / spectral_conv / layer_fwd /
   spectral_conv_adjoint / layer_bwd / gelu / gelu_prime ........ pinned
   decomp.* (partition algebra, decomposition simulator, repartition) pinned
+  network.* (lift, projection, relative-L2 loss, network gradients, Adam)  pinned
+      (tests/test_oracle_network.py)
   equality with the authors' own ``dfno`` code ........... parity unpinned
   (that code is not available; the pins fix our reading of the paper).
 """
 
-from . import spectral, decomp  # noqa: F401
+from . import spectral, decomp, network  # noqa: F401
