@@ -157,6 +157,62 @@ fno_status fno_layer_bwd(fno_plan_t plan, const float* v, const float* z_saved, 
                          const float* dy, const void* R, const float* W, float* dv, void* dR,
                          float* dW, float* db, int accumulate, void* stream);
 
+/* ---- whole network (PAPER.md "Full Network") ---- */
+/*   a1   = W_t a + b_t            time affine, input a has a time axis of size 1
+ *   nu_0 = W_c a1 + b_c           channel affine C_in -> C
+ *   nu_{k+1} = sigma(W nu_k + S nu_k), k < K, no sigma after the last block       P:161-166 (N1b)
+ *   u    = W_p nu_K (+ b_p)       projection C -> 1                                P:171-173 (N1c)
+ *   L    = ||u - y||_2 / ||y||_2  relative L2 misfit over all ranks
+ * All pointers are device pointers on the plan's device, caller-owned; shapes
+ * use the plan's local box: a [B][C_in][Xl][Yl][Z] (the size-1 time axis
+ * dropped), nu / z / scratch [B][C][Xl][Yl][Z][T], u / y [B][1][Xl][Yl][Z][T].
+ * The calls are stream-ordered and, for P > 1, collective (W_t, b_t, W_c, b_c,
+ * W_p, b_p are replicated; their gradients come back summed over ranks in rank
+ * order, the broadcast adjoint P:64; R is kz-owned as in fno_layer_*). */
+#define FNO_NET_MAXK 16
+typedef struct {
+  int32_t layers;       /* K, 1 <= K <= FNO_NET_MAXK */
+  int32_t in_channels;  /* C_in, 1..4 (2 in the paper's CO2 example) */
+  int32_t proj_bias;    /* 1: u = W_p nu_K + b_p; 0: no projection bias */
+} fno_net_desc;
+typedef struct {
+  float* Wt;                   /* [T]  (W_t is T x 1) */
+  float* bt;                   /* [T] */
+  float* Wc;                   /* [C][C_in] */
+  float* bc;                   /* [C] */
+  void* R[FNO_NET_MAXK];       /* float2 [C][C][2mx][2my][nkz][mt] per block */
+  float* W[FNO_NET_MAXK];      /* [C][C] (C_out, C_in) per block */
+  float* b[FNO_NET_MAXK];      /* [C] per block */
+  float* Wp;                   /* [C] */
+  float* bp;                   /* [1]; unused when proj_bias == 0 */
+} fno_net_params;              /* also the layout of the gradients */
+typedef struct {
+  float* nu[FNO_NET_MAXK + 1]; /* nu_0 .. nu_K, written by fno_net_fwd */
+  float* z[FNO_NET_MAXK];      /* pre-activations of blocks 0 .. K-2 (block K-1 has none) */
+  void* vhat[FNO_NET_MAXK];    /* V^ per block, fno_plan_vhat_elems complex each */
+} fno_net_acts;
+/* Bytes of device scratch ("net workspace") fno_net_loss / fno_net_bwd need. */
+fno_status fno_net_workspace_size(fno_plan_t plan, const fno_net_desc* desc, size_t* bytes);
+/* Forward: lift, the K blocks (training mode: z and V^ kept), projection. */
+fno_status fno_net_fwd(fno_plan_t plan, const fno_net_desc* desc, const fno_net_params* params, const float* a,
+                       const fno_net_acts* acts, float* u, void* stream);
+/* loss3 (device, 3 floats) = {L, ||u - y||^2, ||y||^2} over all ranks (fp64
+ * partial sums in a fixed order); the fp64 sums stay in net_ws for fno_net_bwd. */
+fno_status fno_net_loss(fno_plan_t plan, const float* u, const float* y, float* loss3, void* net_ws, void* stream);
+/* Backward of L through projection, blocks and lift (after fno_net_loss on the
+ * same u, y and net_ws).  grads: same layout as params (grads->bp ignored when
+ * proj_bias == 0); every gradient is overwritten.  scratch0 / scratch1: two
+ * field buffers for the adjoint ping-pong. */
+fno_status fno_net_bwd(fno_plan_t plan, const fno_net_desc* desc, const fno_net_params* params, const float* a,
+                       const fno_net_acts* acts, const float* u, const float* y, const fno_net_params* grads,
+                       float* scratch0, float* scratch1, void* net_ws, void* stream);
+/* One Adam step (Kingma & Ba, bias-corrected; P:187 uses lr 1e-3) on n floats:
+ * m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; p -= lr (m/(1-b1^step)) /
+ * (sqrt(v/(1-b2^step)) + eps).  Complex R is passed as 2n floats (real and
+ * imaginary parts updated independently, reading N1d).  step >= 1. */
+fno_status fno_adam(float* p, const float* g, float* m, float* v, size_t n, float lr, float beta1, float beta2,
+                    float eps, int step, void* stream);
+
 /* ---- repartition R_{P->Q} -------------------------------------- */
 /* Moves a tensor of `ndim` <= 8 dimensions and global shape `global_shape`
  * from the Cartesian partition src_pgrid to dst_pgrid over the ranks of comm

@@ -39,6 +39,24 @@ class _Problem(ctypes.Structure):
                 ("modes", ctypes.c_int32 * 4), ("pgrid", ctypes.c_int32 * 2), ("flags", ctypes.c_uint32)]
 
 
+NET_MAXK = 16
+
+
+class _NetDesc(ctypes.Structure):
+    _fields_ = [("layers", ctypes.c_int32), ("in_channels", ctypes.c_int32), ("proj_bias", ctypes.c_int32)]
+
+
+class _NetParams(ctypes.Structure):
+    _fields_ = [("Wt", ctypes.c_void_p), ("bt", ctypes.c_void_p), ("Wc", ctypes.c_void_p), ("bc", ctypes.c_void_p),
+                ("R", ctypes.c_void_p * NET_MAXK), ("W", ctypes.c_void_p * NET_MAXK), ("b", ctypes.c_void_p * NET_MAXK),
+                ("Wp", ctypes.c_void_p), ("bp", ctypes.c_void_p)]
+
+
+class _NetActs(ctypes.Structure):
+    _fields_ = [("nu", ctypes.c_void_p * (NET_MAXK + 1)), ("z", ctypes.c_void_p * NET_MAXK),
+                ("vhat", ctypes.c_void_p * NET_MAXK)]
+
+
 _lib = None
 
 
@@ -72,6 +90,11 @@ def lib() -> ctypes.CDLL:
             "fno_layer_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
             "fno_repartition": [vp, i32, P(ctypes.c_int64), P(ctypes.c_int32), P(ctypes.c_int32), sz, vp, vp, vp,
                                 P(sz), vp],
+            "fno_net_workspace_size": [vp, P(_NetDesc), P(sz)],
+            "fno_net_fwd": [vp, P(_NetDesc), P(_NetParams), vp, P(_NetActs), vp, vp],
+            "fno_net_loss": [vp, vp, vp, vp, vp, vp],
+            "fno_net_bwd": [vp, P(_NetDesc), P(_NetParams), vp, P(_NetActs), vp, vp, P(_NetParams), vp, vp, vp, vp],
+            "fno_adam": [vp, vp, vp, vp, sz, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -317,6 +340,71 @@ def layer_bwd(plan: Plan, v, z_saved, vhat_saved, dy, R, W, dv, dR, dW, db=None,
     _check(lib().fno_layer_bwd(plan.handle, _ptr(v), _ptr(z_saved), _ptr(vhat_saved), _ptr(dy), _ptr(R), _ptr(W),
                                _ptr(dv), _ptr(dR), _ptr(dW), _ptr(db), int(bool(accumulate)), _stream(stream)),
            "fno_layer_bwd")
+
+
+# ---- whole network (fno_net_*) --------------------------------
+
+def _net_desc(layers: int, in_channels: int, proj_bias: bool) -> _NetDesc:
+    return _NetDesc(int(layers), int(in_channels), int(bool(proj_bias)))
+
+
+def _net_params(P: dict) -> _NetParams:
+    """P: Wt [T], bt [T], Wc [C, Cin], bc [C], R/W/b lists, Wp [C], bp [1] or None."""
+    c = _NetParams()
+    c.Wt, c.bt, c.Wc, c.bc = _ptr(P["Wt"]), _ptr(P["bt"]), _ptr(P["Wc"]), _ptr(P["bc"])
+    for k in range(len(P["R"])):
+        c.R[k], c.W[k], c.b[k] = _ptr(P["R"][k]), _ptr(P["W"][k]), _ptr(P["b"][k])
+    c.Wp, c.bp = _ptr(P["Wp"]), _ptr(P.get("bp"))
+    return c
+
+
+def _net_acts(A: dict) -> _NetActs:
+    c = _NetActs()
+    for k, t in enumerate(A["nu"]):
+        c.nu[k] = _ptr(t)
+    for k, t in enumerate(A["z"]):
+        c.z[k] = _ptr(t)
+    for k, t in enumerate(A["vhat"]):
+        c.vhat[k] = _ptr(t)
+    return c
+
+
+def net_workspace_size(plan: Plan, layers: int, in_channels: int, proj_bias: bool = True) -> int:
+    d = _net_desc(layers, in_channels, proj_bias)
+    n = ctypes.c_size_t()
+    _check(lib().fno_net_workspace_size(plan.handle, ctypes.byref(d), ctypes.byref(n)), "fno_net_workspace_size")
+    return n.value
+
+
+def net_fwd(plan: Plan, params: dict, a, acts: dict, u, in_channels: int, proj_bias: bool = True, stream=None):
+    """Lift, K blocks, projection."""
+    d = _net_desc(len(params["R"]), in_channels, proj_bias)
+    cp, ca = _net_params(params), _net_acts(acts)
+    _check(lib().fno_net_fwd(plan.handle, ctypes.byref(d), ctypes.byref(cp), _ptr(a), ctypes.byref(ca), _ptr(u),
+                             _stream(stream)), "fno_net_fwd")
+
+
+def net_loss(plan: Plan, u, y, loss3, net_ws, stream=None):
+    """loss3 = {||u - y|| / ||y||, ||u - y||^2, ||y||^2} over all ranks."""
+    _check(lib().fno_net_loss(plan.handle, _ptr(u), _ptr(y), _ptr(loss3), _ptr(net_ws), _stream(stream)),
+           "fno_net_loss")
+
+
+def net_bwd(plan: Plan, params: dict, a, acts: dict, u, y, grads: dict, scratch0, scratch1, net_ws, in_channels: int,
+            proj_bias: bool = True, stream=None):
+    """Gradient of the loss w.r.t. every parameter (after net_loss on the same u, y, net_ws)."""
+    d = _net_desc(len(params["R"]), in_channels, proj_bias)
+    cp, ca, cg = _net_params(params), _net_acts(acts), _net_params(grads)
+    _check(lib().fno_net_bwd(plan.handle, ctypes.byref(d), ctypes.byref(cp), _ptr(a), ctypes.byref(ca), _ptr(u),
+                             _ptr(y), ctypes.byref(cg), _ptr(scratch0), _ptr(scratch1), _ptr(net_ws), _stream(stream)),
+           "fno_net_bwd")
+
+
+def adam(p, g, m, v, step: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+    """One Adam step on a float32 (or complex64, as 2n floats) tensor."""
+    n = p.numel() * (2 if p.is_complex() else 1)
+    _check(lib().fno_adam(_ptr(p), _ptr(g), _ptr(m), _ptr(v), n, lr, beta1, beta2, eps, int(step), _stream(stream)),
+           "fno_adam")
 
 
 def repartition(comm: Optional[Comm], global_shape, src_pgrid, dst_pgrid, src_local, dst_local, stream=None):

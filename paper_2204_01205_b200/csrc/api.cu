@@ -799,6 +799,194 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
 }
 
 // ---------------------------------------------------------------------------
+// whole network
+// ---------------------------------------------------------------------------
+namespace {
+
+// net workspace layout (bytes offsets), sized for the plan's local box
+struct NetWs {
+  size_t dloss, sums, dall, lparts, pparts, row, rall, total;
+  int gl, gp, gb, plen;
+};
+
+NetWs net_ws_layout(fno_plan_t p, int Cin) {
+  NetParams q{};
+  q.B = p->B; q.C = p->C; q.Cin = Cin; q.T = int(p->T); q.NS = p->Xl * p->Yl * p->Z;
+  NetWs w{};
+  w.gl = net_loss_grid(q, p->num_sms);
+  w.gp = net_proj_bwd_grid(q, p->num_sms);
+  w.gb = net_lift_bwd_grid(q, p->num_sms);
+  w.plen = p->C * Cin + p->C + 2 * int(p->T);
+  const int rlen = std::max(w.plen, p->C + 1);
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off += align256(b); return o; };
+  w.dloss = take(size_t(w.gl) * 2 * sizeof(double));
+  w.sums = take(4 * sizeof(double));
+  w.dall = take(size_t(p->P) * 2 * sizeof(double));
+  w.lparts = take(size_t(w.gb) * w.plen * sizeof(float));
+  w.pparts = take(size_t(w.gp) * (p->C + 1) * sizeof(float));
+  w.row = take(size_t(rlen) * sizeof(float));
+  w.rall = take(size_t(p->P) * rlen * sizeof(float));
+  w.total = off;
+  return w;
+}
+
+fno_status net_check(fno_plan_t p, const fno_net_desc* d, const char* who) {
+  FNO_TRY(check_ready(p, who));
+  if (!d || d->layers < 1 || d->layers > FNO_NET_MAXK || d->in_channels < 1 || d->in_channels > 4)
+    return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": need 1 <= layers <= FNO_NET_MAXK and 1 <= in_channels <= 4");
+  if (p->C > 32) return fail(FNO_ERR_PLAN, std::string(who) + ": the network kernels support width C <= 32");
+  return FNO_OK;
+}
+
+NetParams net_base(fno_plan_t p, int Cin) {
+  NetParams q{};
+  q.B = p->B; q.C = p->C; q.Cin = Cin; q.T = int(p->T); q.NS = p->Xl * p->Yl * p->Z;
+  return q;
+}
+
+// the replicated-parameter gradient row `row` (len floats, this rank's sum)
+// summed over ranks in rank order into `out` (len floats); P == 1: copy
+fno_status net_rank_sum(fno_plan_t p, float* row, int len, float* rall, float* out, cudaStream_t st) {
+  if (p->P == 1) {
+    FNO_CUDA(cudaMemcpyAsync(out, row, size_t(len) * sizeof(float), cudaMemcpyDeviceToDevice, st), "net: gradient copy");
+    return FNO_OK;
+  }
+  FNO_NCCL(ncclAllGather(row, rall, size_t(len), ncclFloat, p->comm->nccl, st), "net: gradient all-gather");
+  FNO_CUDA(launch_rowsum_strided(rall, p->P, len, len, out, 0, st), "net: rank-ordered gradient sum");
+  g_launches++;
+  return FNO_OK;
+}
+
+// runs one block with the activation of its position (GELU except the last)
+struct ActScope {
+  fno_plan_t p;
+  int saved;
+  ActScope(fno_plan_t p_, int act) : p(p_), saved(p_->act_gelu) { p->act_gelu = act; }
+  ~ActScope() { p->act_gelu = saved; }
+};
+
+}  // namespace
+
+extern "C" fno_status fno_net_workspace_size(fno_plan_t p, const fno_net_desc* d, size_t* bytes) {
+  if (!p || !d || !bytes) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_workspace_size: NULL argument");
+  if (d->in_channels < 1 || d->in_channels > 4) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_workspace_size: 1 <= in_channels <= 4");
+  *bytes = net_ws_layout(p, d->in_channels).total;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_net_fwd(fno_plan_t p, const fno_net_desc* d, const fno_net_params* w, const float* a,
+                                  const fno_net_acts* acts, float* u, void* stream) {
+  FNO_TRY(net_check(p, d, "fno_net_fwd"));
+  if (!w || !a || !acts || !u || !w->Wt || !w->bt || !w->Wc || !w->bc || !w->Wp || (d->proj_bias && !w->bp))
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_fwd: NULL argument");
+  const int K = d->layers;
+  for (int k = 0; k <= K; ++k)
+    if (!acts->nu[k]) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_fwd: acts->nu[k] is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NetParams q = net_base(p, d->in_channels);
+  q.a = a; q.Wt = w->Wt; q.bt = w->bt; q.Wc = w->Wc; q.bc = w->bc; q.nu = acts->nu[0];
+  FNO_CUDA(launch_net_lift_fwd(q, p->num_sms, st), "net: lift");
+  g_launches++;
+  for (int k = 0; k < K; ++k) {
+    const int act = k < K - 1 ? 1 : 0;
+    if (act && !acts->z[k]) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_fwd: acts->z[k] is NULL for a GELU block");
+    ActScope as(p, act);
+    FNO_TRY(fno_layer_fwd(p, acts->nu[k], w->R[k], w->W[k], w->b[k], acts->nu[k + 1], act ? acts->z[k] : nullptr,
+                          acts->vhat[k], stream));
+  }
+  q.nu = acts->nu[K]; q.Wp = w->Wp; q.bp = d->proj_bias ? w->bp : nullptr; q.u = u;
+  FNO_CUDA(launch_net_proj_fwd(q, p->num_sms, st), "net: projection");
+  g_launches++;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_net_loss(fno_plan_t p, const float* u, const float* y, float* loss3, void* net_ws, void* stream) {
+  FNO_TRY(check_ready(p, "fno_net_loss"));
+  if (!u || !y || !loss3 || !net_ws) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_loss: NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const NetWs L = net_ws_layout(p, 1);
+  char* ws = static_cast<char*>(net_ws);
+  NetParams q = net_base(p, 1);
+  q.u = const_cast<float*>(u); q.y = y; q.dparts = reinterpret_cast<double*>(ws + L.dloss);
+  double* sums = reinterpret_cast<double*>(ws + L.sums);
+  FNO_CUDA(launch_net_loss_partial(q, L.gl, st), "net: loss partial sums");
+  g_launches++;
+  if (p->P == 1) {
+    FNO_CUDA(launch_net_loss_finalize(q.dparts, L.gl, sums, loss3, st), "net: loss");
+    g_launches++;
+  } else {
+    double* dall = reinterpret_cast<double*>(ws + L.dall);
+    FNO_CUDA(launch_net_loss_finalize(q.dparts, L.gl, dall + 2 * p->rank, nullptr, st), "net: local loss sums");
+    g_launches++;
+    FNO_NCCL(ncclAllGather(dall + 2 * p->rank, dall, 2, ncclDouble, p->comm->nccl, st), "net: loss all-gather");
+    FNO_CUDA(launch_net_loss_finalize(dall, p->P, sums, loss3, st), "net: loss (rank order)");
+    g_launches++;
+  }
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_net_bwd(fno_plan_t p, const fno_net_desc* d, const fno_net_params* w, const float* a,
+                                  const fno_net_acts* acts, const float* u, const float* y, const fno_net_params* g,
+                                  float* s0, float* s1, void* net_ws, void* stream) {
+  FNO_TRY(net_check(p, d, "fno_net_bwd"));
+  if (!w || !a || !acts || !u || !y || !g || !s0 || !s1 || !net_ws || !g->Wt || !g->bt || !g->Wc || !g->bc || !g->Wp ||
+      (d->proj_bias && !g->bp))
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_bwd: NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int K = d->layers, Cin = d->in_channels, C = p->C, T = int(p->T);
+  // the fp64 loss sums of fno_net_loss sit at the same offset for every C_in
+  const NetWs L = net_ws_layout(p, Cin);
+  char* ws = static_cast<char*>(net_ws);
+  float* row = reinterpret_cast<float*>(ws + L.row);
+  float* rall = reinterpret_cast<float*>(ws + L.rall);
+  NetParams q = net_base(p, Cin);
+  // projection + loss adjoint -> dnu_K (s0), dWp, dbp
+  q.u = const_cast<float*>(u); q.y = y; q.nu = acts->nu[K]; q.Wp = w->Wp; q.dnu = s0;
+  q.parts = reinterpret_cast<float*>(ws + L.pparts); q.stats = reinterpret_cast<const double*>(ws + L.sums);
+  FNO_CUDA(launch_net_proj_bwd(q, L.gp, st), "net: projection / loss adjoint");
+  g_launches++;
+  FNO_CUDA(launch_rowsum_strided(q.parts, L.gp, C + 1, C + 1, row, 0, st), "net: dWp / dbp partial sum");
+  g_launches++;
+  FNO_TRY(net_rank_sum(p, row, C, rall, g->Wp, st));
+  if (d->proj_bias) FNO_TRY(net_rank_sum(p, row + C, 1, rall, g->bp, st));
+  // blocks, last to first (ping-pong s0 -> s1 -> s0 ...)
+  float* dcur = s0;
+  float* dnext = s1;
+  for (int k = K - 1; k >= 0; --k) {
+    const int act = k < K - 1 ? 1 : 0;
+    ActScope as(p, act);
+    FNO_TRY(fno_layer_bwd(p, acts->nu[k], act ? acts->z[k] : nullptr, acts->vhat[k], dcur, w->R[k], w->W[k], dnext,
+                          g->R[k], g->W[k], g->b[k], 0, stream));
+    std::swap(dcur, dnext);
+  }
+  // lift adjoint -> dWc, dbc, dWt, dbt
+  q.a = a; q.Wt = w->Wt; q.bt = w->bt; q.Wc = w->Wc; q.dnu = dcur;
+  q.parts = reinterpret_cast<float*>(ws + L.lparts); q.plen = L.plen;
+  FNO_CUDA(launch_net_lift_bwd(q, L.gb, st), "net: lift adjoint");
+  g_launches++;
+  FNO_CUDA(launch_rowsum_strided(q.parts, L.gb, L.plen, L.plen, row, 0, st), "net: lift gradient partial sum");
+  g_launches++;
+  FNO_TRY(net_rank_sum(p, row, C * Cin, rall, g->Wc, st));
+  FNO_TRY(net_rank_sum(p, row + C * Cin, C, rall + size_t(p->P) * C * Cin, g->bc, st));
+  FNO_TRY(net_rank_sum(p, row + C * Cin + C, T, rall + size_t(p->P) * (C * Cin + C), g->Wt, st));
+  FNO_TRY(net_rank_sum(p, row + C * Cin + C + T, T, rall + size_t(p->P) * (C * Cin + C + T), g->bt, st));
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_adam(float* prm, const float* grad, float* m, float* v, size_t n, float lr, float beta1,
+                               float beta2, float eps, int step, void* stream) {
+  if (n == 0) return FNO_OK;
+  if (!prm || !grad || !m || !v || step < 1) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_adam: NULL pointer or step < 1");
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  FNO_CUDA(launch_adam(prm, grad, m, v, (long long)n, lr, beta1, beta2, eps, step, sms, static_cast<cudaStream_t>(stream)),
+           "adam");
+  g_launches++;
+  return FNO_OK;
+}
+
+// ---------------------------------------------------------------------------
 // general repartition R_{P->Q}
 // ---------------------------------------------------------------------------
 namespace {

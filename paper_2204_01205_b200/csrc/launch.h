@@ -63,6 +63,36 @@ cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st);
 cudaError_t launch_rowsum(const float* parts, int nparts, int len, int split, float* out0, float* out1, int accumulate,
                           cudaStream_t st);
 
+// whole-network kernels (network.cu)
+struct NetParams {
+  int B, C, Cin, T;
+  long long NS;                          // local spatial points Xl*Yl*Z
+  const float* a;                        // input [B][Cin][NS] (time axis of size 1)
+  const float *Wt, *bt, *Wc, *bc;        // lift
+  const float *Wp, *bp;                  // projection (bp nullable)
+  float* nu;                             // lift out / projection in / adjoint source
+  float* u;                              // projection out
+  const float* y;                        // target
+  float* dnu;                            // adjoint field
+  float* parts;                          // per-CTA float partials
+  int plen;                              // partial row length
+  double* dparts;                        // per-CTA fp64 partials (loss)
+  const double* stats;                   // {||u - y||^2, ||y||^2} (global)
+};
+cudaError_t launch_net_lift_fwd(const NetParams& q, int num_sms, cudaStream_t st);
+cudaError_t launch_net_proj_fwd(const NetParams& q, int num_sms, cudaStream_t st);
+int net_loss_grid(const NetParams& q, int num_sms);
+cudaError_t launch_net_loss_partial(const NetParams& q, int grid, cudaStream_t st);
+cudaError_t launch_net_loss_finalize(const double* parts, int nrows, double* sums, float* out, cudaStream_t st);
+int net_proj_bwd_grid(const NetParams& q, int num_sms);
+cudaError_t launch_net_proj_bwd(const NetParams& q, int grid, cudaStream_t st);
+int net_lift_bwd_grid(const NetParams& q, int num_sms);
+cudaError_t launch_net_lift_bwd(const NetParams& q, int grid, cudaStream_t st);
+cudaError_t launch_rowsum_strided(const float* rows, int nrows, long long stride, int len, float* out, int acc,
+                                  cudaStream_t st);
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
+                        float eps, int step, int num_sms, cudaStream_t st);
+
 bool ac_pair_supported(int LZ, int LT);
 bool b_size_supported(int L);
 
