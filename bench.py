@@ -217,6 +217,15 @@ def run_ours(args, rank, world, local_rank):
         Rs.append(torch.from_numpy(R).to(dev))
         Ws.append(torch.from_numpy(W).to(dev))
         bs.append(torch.from_numpy(b).to(dev))
+    net = None
+    if args.network:
+        # whole network: input a [B][2][X][Y][Z] (permeability-, topography-like
+        # channels), target y [B][1][X][Y][Z][T]; seeded, CO2-shaped
+        from paper_2204_01205_b200.network import Network
+        net = Network(plan, layers=L, in_channels=2, seed=CONFIG_INDEX)
+        a_in = synth.field_torch((B, 2) + tuple(local[2:5]) + (1,), tuple(modes[:3]) + (1,), seed + 11, "co2",
+                                 device=dev)[..., 0].contiguous()
+        y_t = synth.field_torch((B, 1) + tuple(local[2:]), modes, seed + 12, "co2", device=dev)
     acts = [v0] + [torch.empty_like(v0) for _ in range(L)]
     zs = [torch.empty_like(v0) for _ in range(L)]
     vhs = [torch.empty(plan.vhat_shape(), dtype=torch.complex64, device=dev) for _ in range(L)]
@@ -226,6 +235,9 @@ def run_ours(args, rank, world, local_rank):
     g = [dy, torch.empty_like(v0), torch.empty_like(v0)]
 
     def step():
+        if net is not None:
+            net.train_step(a_in, y_t, lr=1e-3)
+            return
         for l in range(L):
             fno.layer_fwd(plan, acts[l], Rs[l], Ws[l], bs[l], acts[l + 1], zs[l], vhs[l])
         cur = 0                      # g[0] = upstream dy; dv ping-pongs between g[1], g[2]
@@ -280,7 +292,19 @@ def run_ours(args, rank, world, local_rank):
     h_out = torch.empty((L, C * C + C), dtype=torch.float32, pin_memory=True)
     res = torch.empty((L, C * C + C), device=dev)
 
+    if net is not None:     # network: input a and target y in, the loss out
+        h_v = torch.empty(a_in.shape, dtype=torch.float32, pin_memory=True)
+        h_dy = torch.empty(y_t.shape, dtype=torch.float32, pin_memory=True)
+        h_v.copy_(a_in.cpu())
+        h_dy.copy_(y_t.cpu())
+        h_out = torch.empty(3, dtype=torch.float32, pin_memory=True)
+
     def e2e_step():
+        if net is not None:
+            a_in.copy_(h_v, non_blocking=True)
+            y_t.copy_(h_dy, non_blocking=True)
+            h_out.copy_(net.train_step(a_in, y_t, lr=1e-3), non_blocking=True)
+            return
         acts[0].copy_(h_v, non_blocking=True)
         g[0].copy_(h_dy, non_blocking=True)
         step()
@@ -326,7 +350,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ---
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and net is None:
         cpu = oracle_sample(args, v0.detach().cpu().numpy(), dy.detach().cpu().numpy(), modes, repeats=1)
 
     clocks = sampler.summary()
@@ -335,7 +359,10 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": f"synthetic (seeded {'CO2' if cfg['shape'] == 'co2' else 'NS'}-shaped fields, random-init weights)",
-        "config": {"workload": WORKLOADS[cfg["name"]],
+        "config": {"workload": (WORKLOADS[cfg["name"]] if net is None else
+                                f"{cfg['name']}-net: whole DFNO training step (lift 2->{C} channels and 1->{T} "
+                                f"time steps, {L} blocks, projection {C}->1, relative-L2 loss, backward, Adam; "
+                                f"SURVEY 8.f N1) on the {cfg['name']} grid"),
                    "global_grid": list(grid), "pgrid": [px, py], "batch": B, "width": C, "modes": list(modes),
                    "layers": L, "parallelism": f"x/y domain decomposition {px}x{py}",
                    "l2": f"inputs larger than L2 ({B * C * int(np.prod(local[2:])) * 4 / 1e6:.0f} MB field per "
@@ -436,6 +463,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--network", action="store_true",
+                    help="time the whole network's training step (lift, blocks, projection, loss, backward, Adam)")
     ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c2",
                     help="BASELINE.json workload (default c2 = configs[1]; c3 strong, c4 weak, c5 strong)")
     args = ap.parse_args()

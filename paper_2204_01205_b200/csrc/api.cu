@@ -836,6 +836,8 @@ fno_status net_check(fno_plan_t p, const fno_net_desc* d, const char* who) {
   if (!d || d->layers < 1 || d->layers > FNO_NET_MAXK || d->in_channels < 1 || d->in_channels > 4)
     return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": need 1 <= layers <= FNO_NET_MAXK and 1 <= in_channels <= 4");
   if (p->C > 32) return fail(FNO_ERR_PLAN, std::string(who) + ": the network kernels support width C <= 32");
+  if ((p->Xl * p->Yl * p->Z * p->T) % 4 != 0)
+    return fail(FNO_ERR_PLAN, std::string(who) + ": the network kernels need Xl*Yl*Z*T to be a multiple of 4");
   return FNO_OK;
 }
 

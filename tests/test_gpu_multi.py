@@ -51,3 +51,30 @@ def test_decomposed_matches_single_and_oracle(case, peer, tmp_path):
             assert v < 1e-5, (k, v, res)
     for f in res["repartition"]:
         assert f["repart_fwd_exact"] and f["repart_roundtrip_exact"], res
+
+
+# whole network: decomposed fno_net_* == fp64 network oracle
+NET_CASES = [((2, 1), [16, 16, 16, 8], 4, [4, 4, 4, 4], "1"),
+             ((1, 2), [16, 16, 16, 8], 4, [4, 2, 4, 4], "0"),
+             ((2, 2), [16, 16, 32, 16], 6, [4, 4, 8, 8], "1")]
+
+
+@pytest.mark.parametrize("case", NET_CASES, ids=lambda c: f"net_pg{c[0][0]}x{c[0][1]}_peer{c[4]}")
+def test_decomposed_network_matches_oracle(case, tmp_path):
+    pg, grid, C, modes, peer = case
+    n = pg[0] * pg[1]
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    from paper_2204_01205_b200 import build
+    build.build()
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29613", os.path.join(ROOT, "tests", "mp_network.py"),
+           "--pgrid", str(pg[0]), str(pg[1]), "--grid", *map(str, grid), "--width", str(C),
+           "--modes", *map(str, modes), "--out", str(out)]
+    env = dict(os.environ, FNO_PEER_EXCHANGE=peer)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    bad = {k: v for k, v in res.items() if k.endswith("_vs_oracle") and not v < 1e-5}
+    assert not bad, bad

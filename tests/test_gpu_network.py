@@ -29,6 +29,7 @@ CASES = [
     ((16, 8, 16, 8), 4, (4, 2, 4, 4), 2, 2, True),
     ((16, 8, 16, 8), 3, (2, 2, 3, 3), 3, 1, False),
     ((16, 16, 64, 32), 20, (8, 8, 8, 8), 4, 2, True),
+    ((8, 8, 32, 30), 6, (4, 4, 6, 6), 2, 3, True),      # T = 30 (c3 class): scalar t path of the lift adjoint
 ]
 
 
