@@ -122,6 +122,22 @@ fno_status fno_plan_set_workspace(fno_plan_t plan, void* dptr, size_t bytes);
  * other's memory, FNO_ERR_CUDA / FNO_ERR_NCCL on a failed mapping or
  * all-gather (the plan then keeps using NCCL send/recv exchanges). */
 fno_status fno_plan_connect_peers(fno_plan_t plan, void* stream);
+/* Caller-side partition of the fields (the paper's App. A 3-D
+ * spatial and temporal partitions): io_pgrid = (px', py', pz', pt')
+ * over the same P ranks (row-major, each extent divisible by its part).  The
+ * compute calls then take and return v, y, u, g, dy, dv in that partition
+ * (this rank's box: fno_plan_io_box) and repartition them to and from the
+ * plan's x/y grid around the layer ("a repartition operator is used to
+ * take the data to a partition of only the x and y dimensions"; two extra
+ * all-to-alls of the full field per call, generalised R_{P->Q}).  z_save
+ * / z_saved stay in the x/y layout (an opaque buffer of the same size).  Must be
+ * called before fno_plan_workspace_size / fno_plan_set_workspace (the workspace
+ * grows by three field buffers and the repartition scratch).  The network calls
+ * (fno_net_*) keep the x/y partition.  (px, py, 1, 1) is the plan's own grid:
+ * no-op. */
+fno_status fno_plan_set_io_partition(fno_plan_t plan, const int32_t io_pgrid[4]);
+/* This rank's box of the io partition: [lo, hi) per X, Y, Z, T. */
+fno_status fno_plan_io_box(fno_plan_t plan, int64_t lo[4], int64_t hi[4]);
 /* Local x/y box of this rank in global coordinates: [lo, hi) per X, Y, Z, T. */
 fno_status fno_plan_local_box(fno_plan_t plan, int64_t lo[4], int64_t hi[4]);
 /* Retained-kz index block [kz_lo, kz_hi) whose weights this rank owns after the
@@ -206,6 +222,11 @@ fno_status fno_net_loss(fno_plan_t plan, const float* u, const float* y, float* 
 fno_status fno_net_bwd(fno_plan_t plan, const fno_net_desc* desc, const fno_net_params* params, const float* a,
                        const fno_net_acts* acts, const float* u, const float* y, const fno_net_params* grads,
                        float* scratch0, float* scratch1, void* net_ws, void* stream);
+/* Data x domain hybrid: in-place NCCL all-reduce of n floats over
+ * the ranks of comm -- the replicas of a domain-decomposed network that hold the
+ * same x/y box of different samples -- summed (average = 0) or averaged
+ * (average = 1), e.g. the gradients after fno_net_bwd.  Stream-ordered, collective. */
+fno_status fno_comm_allreduce(fno_comm_t comm, float* buf, size_t n, int average, void* stream);
 /* One Adam step (Kingma & Ba, bias-corrected; P:187 uses lr 1e-3) on n floats:
  * m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; p -= lr (m/(1-b1^step)) /
  * (sqrt(v/(1-b2^step)) + eps).  Complex R is passed as 2n floats (real and

@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
             "fno_plan_set_workspace": [vp, vp, sz],
             "fno_plan_connect_peers": [vp, vp],
             "fno_plan_local_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
+            "fno_plan_set_io_partition": [vp, P(ctypes.c_int32)],
+            "fno_plan_io_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
             "fno_plan_owned_modes": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "fno_plan_vhat_elems": [vp, P(sz)],
             "fno_spectral_conv_fwd": [vp, vp, vp, vp, vp, vp],
@@ -94,6 +96,7 @@ def lib() -> ctypes.CDLL:
             "fno_net_fwd": [vp, P(_NetDesc), P(_NetParams), vp, P(_NetActs), vp, vp],
             "fno_net_loss": [vp, vp, vp, vp, vp, vp],
             "fno_net_bwd": [vp, P(_NetDesc), P(_NetParams), vp, P(_NetActs), vp, vp, P(_NetParams), vp, vp, vp, vp],
+            "fno_comm_allreduce": [vp, vp, sz, i32, vp],
             "fno_adam": [vp, vp, vp, vp, sz, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, vp],
         }
         for name, args in sig.items():
@@ -193,7 +196,7 @@ class Comm:
         uid = cls.unique_id() if rank == 0 else bytes(128)
         dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
         t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
-        dist.broadcast(t, src=0, group=group)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
         return cls.init(bytes(t.cpu().tolist()), n, rank)
 
     def destroy(self):
@@ -212,13 +215,20 @@ class Plan:
     """fno_plan_t plus its caller-owned workspace (a torch uint8 tensor)."""
 
     def __init__(self, problem: Problem, comm: Optional[Comm] = None, device=None, allocate: bool = True,
-                 peer_exchange: Optional[bool] = None):
+                 peer_exchange: Optional[bool] = None, io_pgrid: Optional[Sequence[int]] = None):
+        """io_pgrid: optional caller-side (px, py, pz, pt) partition of the fields
+        (fno_plan_set_io_partition, App. A 3-D / temporal partitions)."""
         self.problem = problem
         self.comm = comm
         h = ctypes.c_void_p()
         c = problem.to_c()
         _check(lib().fno_plan_create(ctypes.byref(c), comm.handle if comm else None, ctypes.byref(h)), "fno_plan_create")
         self.handle = h
+        self.io_pgrid = None
+        if io_pgrid is not None:
+            arr = (ctypes.c_int32 * 4)(*[int(x) for x in io_pgrid])
+            _check(lib().fno_plan_set_io_partition(h, arr), "fno_plan_set_io_partition")
+            self.io_pgrid = tuple(int(x) for x in io_pgrid)
         self.workspace = None
         if allocate:
             import torch
@@ -254,6 +264,17 @@ class Plan:
         hi = (ctypes.c_int64 * 4)()
         _check(lib().fno_plan_local_box(self.handle, lo, hi), "fno_plan_local_box")
         return list(zip(lo, hi))
+
+    def io_box(self):
+        """This rank's box of the io partition (== local_box without one)."""
+        lo = (ctypes.c_int64 * 4)()
+        hi = (ctypes.c_int64 * 4)()
+        _check(lib().fno_plan_io_box(self.handle, lo, hi), "fno_plan_io_box")
+        return list(zip(lo, hi))
+
+    def io_shape(self):
+        box = self.io_box() if self.io_pgrid is not None else self.local_box()
+        return (self.problem.batch, self.problem.width) + tuple(hi - lo for lo, hi in box)
 
     def owned_modes(self):
         a, b = ctypes.c_int32(), ctypes.c_int32()
@@ -398,6 +419,14 @@ def net_bwd(plan: Plan, params: dict, a, acts: dict, u, y, grads: dict, scratch0
     _check(lib().fno_net_bwd(plan.handle, ctypes.byref(d), ctypes.byref(cp), _ptr(a), ctypes.byref(ca), _ptr(u),
                              _ptr(y), ctypes.byref(cg), _ptr(scratch0), _ptr(scratch1), _ptr(net_ws), _stream(stream)),
            "fno_net_bwd")
+
+
+def comm_allreduce(comm: Comm, t, average: bool = True, stream=None):
+    """In-place NCCL all-reduce (mean or sum) of a float32 / complex64 tensor over comm
+    (data-parallel gradient averaging across replicas)."""
+    n = t.numel() * (2 if t.is_complex() else 1)
+    _check(lib().fno_comm_allreduce(comm.handle, _ptr(t), n, int(bool(average)), _stream(stream)),
+           "fno_comm_allreduce")
 
 
 def adam(p, g, m, v, step: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):

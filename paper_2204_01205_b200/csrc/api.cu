@@ -112,6 +112,10 @@ struct fno_plan_s {
   std::vector<void*> ipc_opened;  // mappings to close at destroy
   size_t n_slab_xy, n_slab_kz, n_h, n_mode;
   int max_grid_c = 0;
+  // caller-side partition of the fields (fno_plan_set_io_partition)
+  int io[4] = {1, 1, 1, 1};
+  bool io_on = false;
+  size_t o_io_a = 0, o_io_b = 0, o_io_c = 0, o_io_ws = 0, io_ws_bytes = 0;
   int dir = 0;  // 0 forward call, 1 backward call (profiling labels)
   Prof prof;
   ~fno_plan_s() {
@@ -724,7 +728,7 @@ fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1
 
 }  // namespace
 
-extern "C" fno_status fno_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
+static fno_status xy_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
                                             void* stream) {
   FNO_TRY(check_ready(p, "fno_spectral_conv_fwd"));
   p->dir = 0;
@@ -738,7 +742,7 @@ extern "C" fno_status fno_spectral_conv_fwd(fno_plan_t p, const float* v, const 
   return FNO_OK;
 }
 
-extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
+static fno_status xy_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
                                             float* dv, void* dR, int accumulate, void* stream) {
   FNO_TRY(check_ready(p, "fno_spectral_conv_bwd"));
   p->dir = 1;
@@ -755,7 +759,7 @@ extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const 
   return FNO_OK;
 }
 
-extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
+static fno_status xy_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
                                     float* z_save, void* vhat_save, void* stream) {
   FNO_TRY(check_ready(p, "fno_layer_fwd"));
   p->dir = 0;
@@ -769,7 +773,7 @@ extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R,
   return FNO_OK;
 }
 
-extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z_saved, const void* vhat_saved,
+static fno_status xy_layer_bwd(fno_plan_t p, const float* v, const float* z_saved, const void* vhat_saved,
                                     const float* dy, const void* R, const float* W, float* dv, void* dR, float* dW,
                                     float* db, int accumulate, void* stream) {
   FNO_TRY(check_ready(p, "fno_layer_bwd"));
@@ -796,6 +800,127 @@ extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z
     FNO_LAUNCH(p, ST_DW, launch_rowsum(all, p->P, len, p->C * p->C, dW, db, accumulate, st), "dW/db rank-ordered sum");
   }
   return FNO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// caller-side partitions other than the plan's x/y grid (App. A
+// 3-D spatial and temporal partitions): every field is repartitioned
+// to the x/y grid on entry and back on exit ("a repartition operator is
+// used to take the data to a partition of only the x and y dimensions")
+// ---------------------------------------------------------------------------
+fno_status io_move(fno_plan_t p, const float* src, float* dst, bool to_xy, cudaStream_t st) {
+  const int64_t shape[6] = {p->B, p->C, p->X, p->Y, p->Z, p->T};
+  const int32_t io6[6] = {1, 1, p->io[0], p->io[1], p->io[2], p->io[3]};
+  const int32_t xy6[6] = {1, 1, p->px, p->py, 1, 1};
+  size_t wsb = p->io_ws_bytes;
+  return fno_repartition(p->comm, 6, shape, to_xy ? io6 : xy6, to_xy ? xy6 : io6, sizeof(float), src, dst,
+                         wsp<void>(p, p->o_io_ws), &wsb, st);
+}
+
+extern "C" fno_status fno_plan_set_io_partition(fno_plan_t p, const int32_t io_pgrid[4]) {
+  if (!p || !io_pgrid) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_io_partition: NULL argument");
+  if (p->ws) return fail(FNO_ERR_INVALID_STATE, "fno_plan_set_io_partition: call before fno_plan_set_workspace");
+  if (p->io_on) return fail(FNO_ERR_INVALID_STATE, "fno_plan_set_io_partition: already set");
+  const long long ext[4] = {p->X, p->Y, p->Z, p->T};
+  long long prod = 1;
+  for (int d = 0; d < 4; ++d) {
+    if (io_pgrid[d] < 1 || ext[d] % io_pgrid[d] != 0)
+      return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_io_partition: every extent must be divisible by its partition");
+    prod *= io_pgrid[d];
+  }
+  if (prod != p->P) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_io_partition: partition size must equal the plan's ranks");
+  for (int d = 0; d < 4; ++d) p->io[d] = io_pgrid[d];
+  if (io_pgrid[0] == p->px && io_pgrid[1] == p->py && io_pgrid[2] == 1 && io_pgrid[3] == 1) return FNO_OK;
+  p->io_on = true;
+  const int64_t shape[6] = {p->B, p->C, p->X, p->Y, p->Z, p->T};
+  const int32_t io6[6] = {1, 1, p->io[0], p->io[1], p->io[2], p->io[3]};
+  const int32_t xy6[6] = {1, 1, p->px, p->py, 1, 1};
+  size_t a = 0, b = 0;
+  FNO_TRY(fno_repartition(p->comm, 6, shape, io6, xy6, sizeof(float), nullptr, nullptr, nullptr, &a, nullptr));
+  FNO_TRY(fno_repartition(p->comm, 6, shape, xy6, io6, sizeof(float), nullptr, nullptr, nullptr, &b, nullptr));
+  const size_t field = align256(size_t(p->B) * p->C * p->Xl * p->Yl * p->Z * p->T * sizeof(float));
+  p->io_ws_bytes = std::max(a, b);
+  p->o_io_a = p->total;
+  p->o_io_b = p->o_io_a + field;
+  p->o_io_c = p->o_io_b + field;
+  p->o_io_ws = p->o_io_c + field;
+  p->total = p->o_io_ws + align256(p->io_ws_bytes);
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_io_box(fno_plan_t p, int64_t lo[4], int64_t hi[4]) {
+  if (!p || !lo || !hi) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_io_box: NULL argument");
+  const long long ext[4] = {p->X, p->Y, p->Z, p->T};
+  int r = p->rank;
+  int coords[4];
+  for (int d = 3; d >= 0; --d) {
+    coords[d] = r % p->io[d];
+    r /= p->io[d];
+  }
+  for (int d = 0; d < 4; ++d) {
+    long long l, h;
+    block_range(ext[d], p->io[d], coords[d], &l, &h);
+    lo[d] = l;
+    hi[d] = h;
+  }
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
+                                            void* stream) {
+  if (!p || !p->io_on) return xy_spectral_conv_fwd(p, v, R, u, vhat_save, stream);
+  FNO_TRY(check_ready(p, "fno_spectral_conv_fwd"));
+  if (!v || !u) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_fwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* va = wsp<float>(p, p->o_io_a);
+  float* ub = wsp<float>(p, p->o_io_b);
+  FNO_TRY(io_move(p, v, va, true, st));
+  FNO_TRY(xy_spectral_conv_fwd(p, va, R, ub, vhat_save, stream));
+  return io_move(p, ub, u, false, st);
+}
+
+extern "C" fno_status fno_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
+                                            float* dv, void* dR, int accumulate, void* stream) {
+  if (!p || !p->io_on) return xy_spectral_conv_bwd(p, g, R, vhat_saved, dv, dR, accumulate, stream);
+  FNO_TRY(check_ready(p, "fno_spectral_conv_bwd"));
+  if (!g) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: NULL g");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* ga = wsp<float>(p, p->o_io_a);
+  float* db = wsp<float>(p, p->o_io_b);
+  FNO_TRY(io_move(p, g, ga, true, st));
+  FNO_TRY(xy_spectral_conv_bwd(p, ga, R, vhat_saved, dv ? db : nullptr, dR, accumulate, stream));
+  if (dv) FNO_TRY(io_move(p, db, dv, false, st));
+  return FNO_OK;
+}
+
+// z_save / z_saved stay in the plan's x/y layout (an opaque buffer of the same size)
+extern "C" fno_status fno_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
+                                    float* z_save, void* vhat_save, void* stream) {
+  if (!p || !p->io_on) return xy_layer_fwd(p, v, R, W, b, y, z_save, vhat_save, stream);
+  FNO_TRY(check_ready(p, "fno_layer_fwd"));
+  if (!v || !y) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_fwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* va = wsp<float>(p, p->o_io_a);
+  float* yb = wsp<float>(p, p->o_io_b);
+  FNO_TRY(io_move(p, v, va, true, st));
+  FNO_TRY(xy_layer_fwd(p, va, R, W, b, yb, z_save, vhat_save, stream));
+  return io_move(p, yb, y, false, st);
+}
+
+extern "C" fno_status fno_layer_bwd(fno_plan_t p, const float* v, const float* z_saved, const void* vhat_saved,
+                                    const float* dy, const void* R, const float* W, float* dv, void* dR, float* dW,
+                                    float* db, int accumulate, void* stream) {
+  if (!p || !p->io_on) return xy_layer_bwd(p, v, z_saved, vhat_saved, dy, R, W, dv, dR, dW, db, accumulate, stream);
+  FNO_TRY(check_ready(p, "fno_layer_bwd"));
+  if (!v || !dy || !dv) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_bwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* va = wsp<float>(p, p->o_io_a);
+  float* dyb = wsp<float>(p, p->o_io_b);
+  float* dvc = wsp<float>(p, p->o_io_c);
+  FNO_TRY(io_move(p, v, va, true, st));
+  FNO_TRY(io_move(p, dy, dyb, true, st));
+  FNO_TRY(xy_layer_bwd(p, va, z_saved, vhat_saved, dyb, R, W, dvc, dR, dW, db, accumulate, stream));
+  return io_move(p, dvc, dv, false, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -836,6 +961,7 @@ fno_status net_check(fno_plan_t p, const fno_net_desc* d, const char* who) {
   if (!d || d->layers < 1 || d->layers > FNO_NET_MAXK || d->in_channels < 1 || d->in_channels > 4)
     return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": need 1 <= layers <= FNO_NET_MAXK and 1 <= in_channels <= 4");
   if (p->C > 32) return fail(FNO_ERR_PLAN, std::string(who) + ": the network kernels support width C <= 32");
+  if (p->io_on) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": the network runs on the plan's x/y partition (no io partition)");
   if ((p->Xl * p->Yl * p->Z * p->T) % 4 != 0)
     return fail(FNO_ERR_PLAN, std::string(who) + ": the network kernels need Xl*Yl*Z*T to be a multiple of 4");
   return FNO_OK;
@@ -894,7 +1020,7 @@ extern "C" fno_status fno_net_fwd(fno_plan_t p, const fno_net_desc* d, const fno
     const int act = k < K - 1 ? 1 : 0;
     if (act && !acts->z[k]) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_net_fwd: acts->z[k] is NULL for a GELU block");
     ActScope as(p, act);
-    FNO_TRY(fno_layer_fwd(p, acts->nu[k], w->R[k], w->W[k], w->b[k], acts->nu[k + 1], act ? acts->z[k] : nullptr,
+    FNO_TRY(xy_layer_fwd(p, acts->nu[k], w->R[k], w->W[k], w->b[k], acts->nu[k + 1], act ? acts->z[k] : nullptr,
                           acts->vhat[k], stream));
   }
   q.nu = acts->nu[K]; q.Wp = w->Wp; q.bp = d->proj_bias ? w->bp : nullptr; q.u = u;
@@ -958,7 +1084,7 @@ extern "C" fno_status fno_net_bwd(fno_plan_t p, const fno_net_desc* d, const fno
   for (int k = K - 1; k >= 0; --k) {
     const int act = k < K - 1 ? 1 : 0;
     ActScope as(p, act);
-    FNO_TRY(fno_layer_bwd(p, acts->nu[k], act ? acts->z[k] : nullptr, acts->vhat[k], dcur, w->R[k], w->W[k], dnext,
+    FNO_TRY(xy_layer_bwd(p, acts->nu[k], act ? acts->z[k] : nullptr, acts->vhat[k], dcur, w->R[k], w->W[k], dnext,
                           g->R[k], g->W[k], g->b[k], 0, stream));
     std::swap(dcur, dnext);
   }
@@ -973,6 +1099,15 @@ extern "C" fno_status fno_net_bwd(fno_plan_t p, const fno_net_desc* d, const fno
   FNO_TRY(net_rank_sum(p, row + C * Cin, C, rall + size_t(p->P) * C * Cin, g->bc, st));
   FNO_TRY(net_rank_sum(p, row + C * Cin + C, T, rall + size_t(p->P) * (C * Cin + C), g->Wt, st));
   FNO_TRY(net_rank_sum(p, row + C * Cin + C + T, T, rall + size_t(p->P) * (C * Cin + C + T), g->bt, st));
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_comm_allreduce(fno_comm_t comm, float* buf, size_t n, int average, void* stream) {
+  if (!comm || !comm->nccl) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_comm_allreduce: NULL communicator");
+  if (n == 0) return FNO_OK;
+  if (!buf) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_comm_allreduce: NULL buffer");
+  FNO_NCCL(ncclAllReduce(buf, buf, n, ncclFloat, average ? ncclAvg : ncclSum, comm->nccl,
+                         static_cast<cudaStream_t>(stream)), "fno_comm_allreduce");
   return FNO_OK;
 }
 

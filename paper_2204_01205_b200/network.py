@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import math
 
-from . import Plan, adam, net_bwd, net_fwd, net_loss, net_workspace_size
+from . import Plan, adam, comm_allreduce, net_bwd, net_fwd, net_loss, net_workspace_size
 
 __all__ = ["Network", "init_params"]
 
@@ -52,9 +52,12 @@ class Network:
     """Parameters, gradients, Adam state and activations of one DFNO on one plan."""
 
     def __init__(self, plan: Plan, layers: int = 4, in_channels: int = 2, seed: int = 0, proj_bias: bool = True,
-                 params: dict | None = None):
+                 params: dict | None = None, dp_comm=None):
+        """dp_comm: optional libfno Comm over the data-parallel replicas (same x/y box,
+        different samples); backward() then averages every gradient over it (N4)."""
         import torch
         self.plan, self.K, self.cin, self.proj_bias = plan, layers, in_channels, proj_bias
+        self.dp_comm = dp_comm
         dev = plan.workspace.device
         self.params = params if params is not None else init_params(plan, layers, in_channels, seed, proj_bias, dev)
         z = lambda t: None if t is None else torch.zeros_like(t)          # noqa: E731
@@ -83,6 +86,11 @@ class Network:
     def backward(self, a, y, stream=None):
         net_bwd(self.plan, self.params, a, self.acts, self.u, y, self.grads, self.scratch[0], self.scratch[1],
                 self.net_ws, self.cin, self.proj_bias, stream)
+        if self.dp_comm is not None:
+            for g in self.grads.values():
+                for t in (g if isinstance(g, list) else [g]):
+                    if t is not None:
+                        comm_allreduce(self.dp_comm, t, True, stream)
 
     def adam_step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
         self.step_count += 1

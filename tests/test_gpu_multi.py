@@ -78,3 +78,52 @@ def test_decomposed_network_matches_oracle(case, tmp_path):
     res = json.loads(out.read_text())
     bad = {k: v for k, v in res.items() if k.endswith("_vs_oracle") and not v < 1e-5}
     assert not bad, bad
+
+
+# data x domain hybrid: gradients averaged over replicas == mean oracle gradient
+HYB_CASES = [(2, (1, 1)), (2, (2, 1))]
+
+
+@pytest.mark.parametrize("case", HYB_CASES, ids=lambda c: f"dp{c[0]}_pg{c[1][0]}x{c[1][1]}")
+def test_data_domain_hybrid_gradients_match_oracle(case, tmp_path):
+    dp, pg = case
+    n = dp * pg[0] * pg[1]
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    from paper_2204_01205_b200 import build
+    build.build()
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29615", os.path.join(ROOT, "tests", "mp_hybrid.py"),
+           "--dp", str(dp), "--pgrid", str(pg[0]), str(pg[1]), "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["replicas_identical"]
+    bad = {k: v for k, v in res.items() if k.endswith("_vs_oracle") and not v < 1e-5}
+    assert not bad, bad
+
+
+# caller-side 3-D spatial / temporal partitions: io partition
+# != the plan's x/y grid, repartitioned around the layer
+IO_CASES = [((2, 1), (1, 1, 2, 1)), ((2, 1), (1, 1, 1, 2)), ((1, 2), (2, 1, 1, 1)),
+            ((2, 2), (1, 2, 2, 1)), ((2, 2), (1, 1, 2, 2))]
+
+
+@pytest.mark.parametrize("case", IO_CASES, ids=lambda c: f"pg{c[0][0]}x{c[0][1]}_io" + "x".join(map(str, c[1])))
+def test_io_partition_layer_matches_oracle(case, tmp_path):
+    pg, io = case
+    n = pg[0] * pg[1]
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    from paper_2204_01205_b200 import build
+    build.build()
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29617", os.path.join(ROOT, "tests", "mp_io.py"),
+           "--pgrid", str(pg[0]), str(pg[1]), "--io", *map(str, io), "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    bad = {k: v for k, v in res.items() if k.endswith("_vs_oracle") and not v < 1e-5}
+    assert not bad, bad
