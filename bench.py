@@ -312,15 +312,53 @@ def run_ours(args, rank, world, local_rank):
         res[:, C * C:].copy_(db)
         h_out.copy_(res, non_blocking=True)
 
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
+    # layer stack: the next step's inputs are copied on a second stream while the
+    # current step computes (two device input slots); each step still moves its
+    # own inputs host -> device and its result device -> host
+    cstream = torch.cuda.Stream(device=dev)
+    vslot = [acts[0], torch.empty_like(acts[0])]
+    dyslot = [g[0], torch.empty_like(g[0])]
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [False, False]
+
+    def prefetch(slot):
+        with torch.cuda.stream(cstream):
+            if used[slot]:
+                cstream.wait_event(consumed[slot])
+            vslot[slot].copy_(h_v, non_blocking=True)
+            dyslot[slot].copy_(h_dy, non_blocking=True)
+            copied[slot].record(cstream)
+
+    def run_e2e(n, start_event=None):
+        if net is not None:
+            for _ in range(n):
+                e2e_step()
+            return
+        if start_event is not None:
+            cstream.wait_event(start_event)
+        prefetch(0)
+        for i in range(n):
+            s = i % 2
+            if i + 1 < n:
+                prefetch(1 - s)
+            stream.wait_event(copied[s])
+            acts[0], g[0] = vslot[s], dyslot[s]
+            step()
+            consumed[s].record(stream)
+            used[s] = True
+            res[:, :C * C].copy_(dW.view(L, C * C))
+            res[:, C * C:].copy_(db)
+            h_out.copy_(res, non_blocking=True)
+
+    run_e2e(max(2, args.warmup))
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    run_e2e(args.steps, e0)
     e1.record(stream)
     e1.synchronize()
+    cstream.synchronize()
     t2 = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
@@ -368,6 +406,8 @@ def run_ours(args, rank, world, local_rank):
                    "l2": f"inputs larger than L2 ({B * C * int(np.prod(local[2:])) * 4 / 1e6:.0f} MB field per "
                          f"layer per GPU; L2 126 MB)"},
         "e2e": {"value": round(e2e_value, 1), "unit": "grid-pts·ch/s", "ms_per_step": round(e2e_ms, 4),
+                "overlap": ("the next step's pinned-host inputs are copied on a second stream while the current step "
+                            "computes (two device input slots)" if net is None else "none"),
                 "h2d_bytes_per_step": int(h_v.numel() * 4 + h_dy.numel() * 4),
                 "d2h_bytes_per_step": int(h_out.numel() * 4)},
         "gpu_launches": int(launches),

@@ -274,11 +274,6 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
     }
     __syncthreads();
     const long long col_next = col + gridDim.x;
-    // the next column's slab rows into L1 (the only L1-allocating loads of the
-    // kernel), so its phase 1 does not stall on L2 / HBM latency
-    if (col_next < p.n_cols)
-      for (int r = tid; r < C * 2 * mz; r += C2T)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(slab_at(col_next, r / (2 * mz), r % (2 * mz))));
 
     for (int ti = 0; ti < tpc; ++ti) {
       const int rz = ti / nch, tc = ti - rz * nch;
