@@ -4,6 +4,8 @@ ownership, workspace sizing) agrees with the partition algebra of the paper
  as pinned in tests/test_oracle_decomp.py.  No compute calls."""
 
 import ctypes
+
+import numpy as np
 import os
 import re
 
@@ -97,3 +99,50 @@ def test_repartition_workspace_query_and_validation(L):
     assert n.value >= 2 * 8 * 6 * 4
     two = (ctypes.c_int32 * 2)(2, 1)
     assert L.fno_repartition(None, 2, shp, one, two, 4, None, None, None, ctypes.byref(n), None) == 1
+
+
+@pytest.mark.parametrize("grid,pg,io", [((16, 16, 16, 8), (2, 1), (1, 1, 2, 1)), ((16, 16, 16, 8), (2, 1), (1, 1, 1, 2)),
+                                        ((32, 16, 64, 30), (2, 2), (1, 2, 2, 1)), ((64, 64, 64, 32), (4, 2), (2, 1, 2, 2)),
+                                        ((16, 16, 16, 8), (2, 2), (2, 2, 1, 1))])
+def test_io_partition_boxes_tile_the_domain(L, grid, pg, io):
+    """fno_plan_set_io_partition: every rank's io box is the
+    balanced block of the row-major (px', py', pz', pt') grid (partition algebra
+    of the oracle), the boxes tile the domain, and the workspace grows by the
+    staging buffers unless io is the plan's own x/y grid."""
+    P = pg[0] * pg[1]
+    cover = np.zeros(grid, dtype=np.int32)
+    for r in range(P):
+        comm = fno.Comm.local(P, r)
+        base = fno.Plan(fno.Problem(grid=grid, width=4, modes=(4, 4, 4, 4), pgrid=pg), comm, allocate=False)
+        plan = fno.Plan(fno.Problem(grid=grid, width=4, modes=(4, 4, 4, 4), pgrid=pg), comm, allocate=False, io_pgrid=io)
+        box = plan.io_box()
+        ref = dc.local_box((1, 4) + tuple(grid), (1, 1) + tuple(io), r)[2:]
+        assert [tuple(b) for b in box] == [tuple(b) for b in ref]
+        cover[tuple(slice(lo, hi) for lo, hi in box)] += 1
+        same = tuple(io) == (pg[0], pg[1], 1, 1)
+        assert (plan.workspace_size() == base.workspace_size()) if same else (plan.workspace_size() > base.workspace_size())
+        plan.destroy()
+        base.destroy()
+        comm.destroy()
+    assert (cover == 1).all()
+
+
+def test_io_partition_validation(L):
+    comm = fno.Comm.local(2, 0)
+    plan = fno.Plan(fno.Problem(grid=(16, 16, 16, 8), width=4, modes=(4, 4, 4, 4), pgrid=(2, 1)), comm, allocate=False)
+    for bad, status in [((1, 1, 1, 1), 1),      # 1 rank != 2
+                        ((1, 1, 3, 1), 1),      # 16 % 3 != 0, and 3 ranks
+                        ((1, 1, 1, 16), 1)]:    # 16 ranks
+        arr = (ctypes.c_int32 * 4)(*bad)
+        assert L.fno_plan_set_io_partition(plan.handle, arr) == status
+    ok = (ctypes.c_int32 * 4)(1, 1, 2, 1)
+    assert L.fno_plan_set_io_partition(plan.handle, ok) == 0
+    assert L.fno_plan_set_io_partition(plan.handle, ok) == 3     # already set
+    plan.destroy()
+    # after the workspace is set: invalid state
+    plan2 = fno.Plan(fno.Problem(grid=(16, 16, 16, 8), width=4, modes=(4, 4, 4, 4)), allocate=False)
+    fno._check(L.fno_plan_set_workspace(plan2.handle, ctypes.c_void_p(1 << 20), plan2.workspace_size()), "set_workspace")
+    one = (ctypes.c_int32 * 4)(1, 1, 1, 1)
+    assert L.fno_plan_set_io_partition(plan2.handle, one) == 3
+    plan2.destroy()
+    comm.destroy()
