@@ -185,3 +185,81 @@ def test_full_size_c2_sampled_outputs():
     assert rel_l2(yg, sp.gelu(z_ref)) < TOL
     del y, z, vh
     torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ci", [3, 4], ids=["c3", "c4"])
+def test_full_size_c3_c4_forward_sampled_outputs(ci):
+    """BASELINE configs[2] (64^3 x 30, m=12: the cp.async / T=30 path) and
+    configs[3] per-GPU box (64x128x128x32, m=12) at full size; the oracle's V^ in
+    full and y, z at 512 sampled points."""
+    import torch
+    from tests import _gpu as G
+    cfg = synth.CONFIGS[ci]
+    grid, C, modes = cfg["grid"], cfg["width"], cfg["modes"]
+    pr = synth.problem(ci, with_dy=False)
+    plan = G.make_plan(grid, C, modes)
+    y, z, vh = G.layer_fwd(plan, pr["v"], pr["R"], pr["W"], pr["b"])
+    v64 = G.f32(pr["v"])
+    vh_ref = sp.forward_modes(v64, modes)
+    assert rel_l2(G.np64(vh), vh_ref) < TOL
+    what = sp.mix(vh_ref, G.f32(pr["R"]))
+    rng = np.random.default_rng(ci)
+    pts = np.stack([rng.integers(0, n, size=512) for n in grid], -1)
+    u_s = sp.inverse_modes_at(what, grid, pts)[0]
+    vs = v64[0][:, pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+    z_ref = G.f32(pr["W"]) @ vs + G.f32(pr["b"])[:, None] + u_s
+    zg = G.np64(z)[0][:, pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+    yg = G.np64(y)[0][:, pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+    assert rel_l2(zg, z_ref) < TOL
+    assert rel_l2(yg, sp.gelu(z_ref)) < TOL
+    del y, z, vh
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_full_size_c2_backward():
+    """The c2 backward at full size (the launch configuration bench.py times):
+    the oracle forms z, dz on the whole grid, then dR, dW, db in full and dv at
+    512 sampled points (dv = W^T dz + S^T dz with S^T by R^H, reading of P:74)."""
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    cfg = synth.CONFIGS[2]
+    grid, C, modes = cfg["grid"], cfg["width"], cfg["modes"]
+    pr = synth.problem(2, with_dy=True)
+    plan = G.make_plan(grid, C, modes)
+    vt, Rt, Wt, bt = G.t32(pr["v"]), G.tc64(pr["R"]), G.t32(pr["W"]), G.t32(pr["b"])
+    y = torch.empty_like(vt)
+    z = torch.empty_like(vt)
+    vh = torch.empty(plan.vhat_shape(), dtype=torch.complex64, device="cuda")
+    fno.layer_fwd(plan, vt, Rt, Wt, bt, y, z, vh)
+    dv = torch.empty_like(vt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.empty((C, C), device="cuda")
+    db = torch.empty((C,), device="cuda")
+    fno.layer_bwd(plan, vt, z, vh, G.t32(pr["dy"]), Rt, Wt, dv, dR, dW, db)
+    torch.cuda.synchronize()
+    del y, z, vh
+    v64, R64, W64, b64, dy64 = G.f32(pr["v"]), G.f32(pr["R"]), G.f32(pr["W"]), G.f32(pr["b"]), G.f32(pr["dy"])
+    _, z_ref = sp.layer_fwd(v64, R64, W64, b64, modes)
+    dz = dy64 * sp.gelu_prime(z_ref)
+    del z_ref
+    vh_ref = sp.forward_modes(v64, modes)
+    gh = sp.forward_modes(dz, modes)
+    X, Y, Z, T = grid
+    cw = sp.c_weight(T, modes[3])
+    dR_ref = np.einsum("bixyzt,boxyzt->ioxyzt", np.conj(vh_ref), gh) * (cw / float(X * Y * Z * T))
+    assert rel_l2(G.np64(dR), dR_ref) < TOL
+    dW_ref = np.einsum("boxyzt,bixyzt->oi", dz, v64)
+    assert rel_l2(G.np64(dW), dW_ref) < TOL
+    assert rel_l2(G.np64(db), dz.sum(axis=(0, 2, 3, 4, 5))) < TOL
+    RH = np.conj(np.swapaxes(R64, 0, 1))
+    wh = sp.mix(gh, RH)
+    rng = np.random.default_rng(11)
+    pts = np.stack([rng.integers(0, n, size=512) for n in grid], -1)
+    sel = (slice(None), pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3])          # [C, P] of batch 0
+    dv_ref = W64.T @ dz[0][sel] + sp.inverse_modes_at(wh, grid, pts)[0]
+    assert rel_l2(G.np64(dv)[0][sel], dv_ref) < TOL
+    del dv, dR
+    torch.cuda.empty_cache()
