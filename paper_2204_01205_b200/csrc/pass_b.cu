@@ -146,14 +146,19 @@ __global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
   const long long total = (long long)p.B * p.nkz * p.C * p.X * p.mt;
   const long long pid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (pid < total) {
+    // thread order (kt, kzl, oc) fastest, then x: for a fixed (x, y) the outputs
+    // of consecutive threads are contiguous in the destination chunk
+    // [B][Xl][Yl][C][nkz][mt], so each warp store is one long run -- these are
+    // the remote NVLink stores of the peer exchange (the reads of the
+    // L2-resident H buffer are the ones that scatter)
     const int kt = int(pid % p.mt);
     long long r = pid / p.mt;
-    const int x = int(r % p.X);
-    r /= p.X;
+    const int kzl = int(r % p.nkz);
+    r /= p.nkz;
     const int oc = int(r % p.C);
     r /= p.C;
-    const int kzl = int(r % p.nkz);
-    const int b = int(r / p.nkz);
+    const int x = int(r % p.X);
+    const int b = int(r / p.X);
     const float2* __restrict__ in = p.in + (((long long)(b * p.nkz + kzl) * p.C + oc) * p.X + x) * my2 * p.mt + kt;
     float2 e[L];
 #pragma unroll
