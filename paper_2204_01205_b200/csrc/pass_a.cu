@@ -194,19 +194,38 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
       const int c = int(r1 % p.C);
       const int b = int(r1 / p.C);
       const long long pt = ((long long)(b * p.Xl + xl) * p.Yl + yl) * p.C + c;  // point-channel index in chunk
+      // rows of mt complex: 16-byte pair stores when mt is even (fewer, wider
+      // stores -- over NVLink when the peer exchange writes the owners' slabs)
+      const bool pairs = (mt & 1) == 0;
       if (kzp < mz) {  // kz = +kz' -> retained index jz = kz'
         float2* o = jbase[kzp] + pt * jnk[kzp] * mt;
+        if (pairs) {
 #pragma unroll
-        for (int i = 0; i < LT; ++i)
-          if (i < mt) o[i] = acc[i];
+          for (int i = 0; i < LT; i += 2)
+            if (i < mt) *reinterpret_cast<float4*>(o + i) = make_float4(acc[i].x, acc[i].y, acc[i + 1].x, acc[i + 1].y);
+        } else {
+#pragma unroll
+          for (int i = 0; i < LT; ++i)
+            if (i < mt) o[i] = acc[i];
+        }
       }
-      if (kzp >= 1) {  // kz = -kz' -> retained index jz = 2mz - kz'
+      if (kzp >= 1) {  // kz = -kz' -> retained index jz = 2mz - kz'; frequency -kt sits in residue (LT - kt) % LT
         const int jz = 2 * mz - kzp;
         float2* o = jbase[jz] + pt * jnk[jz] * mt;
+        if (pairs) {
 #pragma unroll
-        for (int i = 0; i < LT; ++i) {
-          const int kt = (LT - i) % LT;             // residue i holds frequency -kt
-          if (kt < mt && (i == 0 || i > LT - mt)) o[kt] = cconj(acc[i]);
+          for (int kt = 0; kt < LT; kt += 2) {
+            if (kt < mt) {
+              const float2 a0 = cconj(acc[(LT - kt) % LT]), a1 = cconj(acc[(LT - kt - 1) % LT]);
+              *reinterpret_cast<float4*>(o + kt) = make_float4(a0.x, a0.y, a1.x, a1.y);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < LT; ++i) {
+            const int kt = (LT - i) % LT;
+            if (kt < mt && (i == 0 || i > LT - mt)) o[kt] = cconj(acc[i]);
+          }
         }
       }
     }
