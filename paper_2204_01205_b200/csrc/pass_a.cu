@@ -244,7 +244,7 @@ void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* sme
   // stage buffers when three CTAs still fit an SM, else one
   int np = (AT + T - 1) / T;
   if (np < 1) np = 1;
-  const size_t per3 = 74 * 1024;
+  const size_t per3 = 75 * 1024;   // three CTAs per SM: 3 x (75 + 1 reserved) KB <= 228 KB
   int ns = 2;
   ALayout L = a_layout(Z, T, mz, np, mode, ns);
   if (L.total > per3) {
