@@ -194,7 +194,10 @@ __global__ void __launch_bounds__(BT) b_yinv_kernel(PassBParams p) {
 // once, coalesced across the mode-minor threads.  A thread owns one mode m and
 // a chunk of MCH outputs (fwd: o; bwd: i), so the grid has ceil(C / MCH) times
 // more warps in flight than a thread-per-mode kernel.
-constexpr int MCH = 4;
+#ifndef FNO_MCH
+#define FNO_MCH 2
+#endif
+constexpr int MCH = FNO_MCH;
 
 // forward mixing: W^[b,o,m] = sum_i V^[b,i,m] R[i,o,m]
 template <int CMAX>
