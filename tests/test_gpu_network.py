@@ -30,11 +30,12 @@ CASES = [
     ((16, 8, 16, 8), 3, (2, 2, 3, 3), 3, 1, False),
     ((16, 16, 64, 32), 20, (8, 8, 8, 8), 4, 2, True),
     ((8, 8, 32, 30), 6, (4, 4, 6, 6), 2, 3, True),      # T = 30 (c3 class): scalar t path of the lift adjoint
+    ((16, 8, 16, 8), 4, (4, 2, 4, 4), 2, 2, True, 3),    # batch 3: the loss and every sum run over the batch too
 ]
 
 
 def _ids(c):
-    return "x".join(map(str, c[0])) + f"_C{c[1]}_K{c[3]}_Cin{c[4]}_bp{int(c[5])}"
+    return "x".join(map(str, c[0])) + f"_C{c[1]}_K{c[3]}_Cin{c[4]}_bp{int(c[5])}" + (f"_B{c[6]}" if len(c) > 6 else "")
 
 
 @pytest.mark.parametrize("case", CASES, ids=_ids)
@@ -43,11 +44,12 @@ def test_network_forward_loss_gradients_and_adam_match_oracle(case):
     from paper_2204_01205_b200 import Plan, Problem
     from paper_2204_01205_b200.network import Network
     from tests import _gpu as G
-    grid, C, modes, K, Cin, bp = case
+    grid, C, modes, K, Cin, bp = case[:6]
+    B = case[6] if len(case) > 6 else 1
     X, Y, Z, T = grid
-    a = synth.field((1, Cin, X, Y, Z, 1), modes[:3] + (1,), 11, "co2")
-    y = synth.field((1, 1, X, Y, Z, T), modes, 12, "co2")
-    plan = Plan(Problem(grid=grid, width=C, modes=modes))
+    a = synth.field((B, Cin, X, Y, Z, 1), modes[:3] + (1,), 11, "co2")
+    y = synth.field((B, 1, X, Y, Z, T), modes, 12, "co2")
+    plan = Plan(Problem(grid=grid, width=C, modes=modes, batch=B))
     net = Network(plan, layers=K, in_channels=Cin, seed=3, proj_bias=bp)
     at, yt = G.t32(a[..., 0]), G.t32(y)
     u = net.forward(at)
