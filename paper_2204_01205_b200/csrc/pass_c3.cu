@@ -25,7 +25,7 @@ bool pass_c3_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   if (CP > 20) return false;
   if (LZ != 8 && LZ != 16 && LZ != 32) return false;
   const int tch = C3T / LZ;
-  if (T % 4 != 0 || T % tch != 0) return false;
+  if (tch > T) return false;   // T % 4 != 0: cp.async tiles (TMA rows would be misaligned)
   const size_t s = c3_layout(CP, C, Z, T, mz, mt, LZ).total;
   if (s > 227 * 1024) return false;
   *CPo = CP;
@@ -39,8 +39,8 @@ cudaError_t launch_pass_c3(const PassCParams& p0, int LZ, int LT, int CP, int gr
   p.TCH = C3T / LZ;
   C2Maps maps;
   std::memset(&maps, 0, sizeof maps);
-  if (!c2_encode_tile_map(&maps.m[0], p.v, p, LZ)) return cudaErrorInvalidValue;
-  p.use_tma = 1;
+  p.use_tma = (p.T % 4 == 0 && c2_encode_tile_map(&maps.m[0], p.v, p, LZ)) ? 1 : 0;
+  p.VW = (p.T % 2 == 0) ? 2 : 1;   // cp.async piece (floats) of the non-TMA path
   switch (CP) {
     case 4: return launch_pass_c3_cp4(maps, p, LZ, LT, grid, smem, st);
     case 8: return launch_pass_c3_cp8(maps, p, LZ, LT, grid, smem, st);

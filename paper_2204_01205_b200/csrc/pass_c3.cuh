@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
   const int nk = L.nk, TP = L.TP, UPS = L.UPS;
   const long long ZT = (long long)Z * T;
   const long long chan_stride = (long long)p.Xl * p.Yl * ZT;
-  const int nch = T / TCH;
+  const int nch = (T + TCH - 1) / TCH;   // the last t chunk is ragged when T % TCH != 0
   const int tpc = p.Qz * nch;        // tiles per column: ti = rz * nch + t chunk
   const unsigned tile_bytes = unsigned(C) * C3T * sizeof(float);
   const int per_c = 2 * mz * mt;
@@ -207,16 +207,37 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
       const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
       return p.in + p.slab.off[dm.x] + ((c_ * C + c) * nkz + dm.y) * mt;
     };
-    auto issue_tile = [&](long long c_, int ti) {   // one thread
+    // v tile (rz, t chunk tc) of column c_ into X: one TMA (thread 0) when T % 4
+    // == 0, else cp.async row pieces by all transform threads (a z row of T
+    // floats is not 16-byte aligned; the ragged chunk leaves stale columns that
+    // are never stored)
+    auto issue_tile = [&](long long c_, int ti) {   // all transform threads
       const int rz = ti / nch, tc = ti - rz * nch;
       int bb;
       const int xy = col_split(c_, &bb);
-      mbar_expect_tx(&bar[0], tile_bytes);
-      tma_load_5d(X, &maps.m[0], tc * TCH, rz, 0, xy, bb * C, &bar[0]);
+      if (p.use_tma) {
+        if (ttid == 0) {
+          mbar_expect_tx(&bar[0], tile_bytes);
+          tma_load_5d(X, &maps.m[0], tc * TCH, rz, 0, xy, bb * C, &bar[0]);
+        }
+        return;
+      }
+      const int t0 = tc * TCH, tcw = min(TCH, T - t0), VW = p.VW;
+      const int nvec = (tcw + VW - 1) / VW;
+      const float* src = p.v + (long long)bb * C * chan_stride + (long long)xy * ZT + rz * T + t0;
+      for (int e = ttid; e < C * LZ * nvec; e += NTT) {
+        const int row = e / nvec, vv = e - row * nvec;
+        const int c = row / LZ, s = row - c * LZ;
+        const float* g = src + c * chan_stride + (long long)p.Qz * s * T + vv * VW;
+        float* d = X + c * C3T + s * TCH + vv * VW;
+        if (VW == 2) cp_async8(d, g);
+        else cp_async4(d, g);
+      }
+      cp_commit();
     };
     const uint32_t idesc = umma_idesc_tf32(C3T, NP, 0, 0);
     constexpr uint32_t A_LBO = (C3T / 8) * 128, B_LBO = (NP / 8) * 128;
-    if (ttid == 0) issue_tile(blockIdx.x, 0);
+    issue_tile(blockIdx.x, 0);
     unsigned k = 0, tphase = 0u;   // tile counter of this CTA, v-tile barrier parity
     for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
       const long long col_next = col + gridDim.x;
@@ -264,8 +285,13 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         mbar_wait(&bempty[b], (use & 1u) ^ 1u);
         // ---- split the v tile into the K-major tf32 hi / lo operands --------
         if (k > 0) mbar_wait(&bmma[(k - 1) & 1], ((k - 1) >> 1) & 1u);   // MMA k-1 done reading A
-        mbar_wait(&bar[0], tphase);
-        tphase ^= 1u;
+        if (p.use_tma) {
+          mbar_wait(&bar[0], tphase);
+          tphase ^= 1u;
+        } else {
+          cp_wait<0>();
+          group_sync(1, NTT);
+        }
         for (int e = (p.ablate & 2) ? C3T * (CP / 4) : ttid; e < C3T * (CP / 4); e += NTT) {
           const int g = e / C3T, pp = e - g * C3T;
           float4 hi, lo;
@@ -280,9 +306,9 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         }
         fence_proxy_async();   // generic-proxy operand stores -> visible to the tensor core
         group_sync(1, NTT);    // A complete, X free
+        if (ti + 1 < tpc) issue_tile(col, ti + 1);
+        else if (col_next < p.n_cols) issue_tile(col_next, 0);
         if (ttid == 0) {
-          if (ti + 1 < tpc) issue_tile(col, ti + 1);
-          else if (col_next < p.n_cols) issue_tile(col_next, 0);
           tc_fence_after();
           const uint32_t dt = tmem + 32u * b;
 #pragma unroll
@@ -299,8 +325,10 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         }
         float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
         // ---- phase 2: inverse z (real output), items (c, tt) -> U[b] --------
+        const int tcw = min(TCH, T - t0);   // ragged chunk: columns tt >= tcw are never stored
         for (int it = (p.ablate & 1) ? C * TCH : ttid; it < C * TCH; it += NTT) {
           const int c = it / TCH, tt = it - c * TCH;
+          if (tt >= tcw) continue;
           float2 e[LZ];
 #pragma unroll
           for (int i = 0; i < LZ; ++i)
@@ -346,17 +374,30 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         const int pq = 32 * warp + 4 * (lane & 7);
         const int sq = pq / TCH, tq = pq - sq * TCH;
         const long long gq = cbase + (long long)(rz + p.Qz * sq) * T + t0 + tq;
+        const int nv = min(4, T - t0 - tq);   // valid points of this quad (ragged last chunk)
+        const bool v4 = (T % 4 == 0) && nv == 4;
 #pragma unroll
         for (int j = 0; j < (CP + 3) / 4; ++j) {
           const int o = (lane >> 3) + 4 * j;
-          if (o >= C || (p.ablate & 4)) break;
+          if (o >= C || (p.ablate & 4) || nv <= 0) break;
           float4 r = *reinterpret_cast<const float4*>(U + o * UPS + pq);
           const long long g = gq + o * chan_stride;
-          if (p.zsave) __stcs(reinterpret_cast<float4*>(p.zsave + g), r);
-          if (p.act_gelu) {
-            r.x = gelu_f(r.x); r.y = gelu_f(r.y); r.z = gelu_f(r.z); r.w = gelu_f(r.w);
+          if (v4) {
+            if (p.zsave) __stcs(reinterpret_cast<float4*>(p.zsave + g), r);
+            if (p.act_gelu) {
+              r.x = gelu_f(r.x); r.y = gelu_f(r.y); r.z = gelu_f(r.z); r.w = gelu_f(r.w);
+            }
+            __stcs(reinterpret_cast<float4*>(p.out + g), r);
+          } else {
+            const float rv[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kk < nv) {
+                if (p.zsave) p.zsave[g + kk] = rv[kk];
+                p.out[g + kk] = p.act_gelu ? gelu_f(rv[kk]) : rv[kk];
+              }
+            }
           }
-          __stcs(reinterpret_cast<float4*>(p.out + g), r);
         }
         mbar_arrive(&bempty[b]);   // U[b], D[b] free
       }
