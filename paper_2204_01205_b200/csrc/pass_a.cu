@@ -17,6 +17,8 @@
 // (cp.async.bulk, completion on an mbarrier) into one of two stage buffers; the
 // copy of batch k+2 is issued as soon as phase 1 of batch k has drained its
 // buffer, so HBM stays busy while the CTA transforms.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -240,20 +242,36 @@ __global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(Pass
 }
 
 void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* smem, int* use_tma) {
-  // one z-pencil per thread in phase 1: NP = AT / T planes per batch; two
-  // stage buffers when three CTAs still fit an SM, else one
-  int np = (AT + T - 1) / T;
-  if (np < 1) np = 1;
-  const size_t per3 = 75 * 1024;   // three CTAs per SM: 3 x (75 + 1 reserved) KB <= 228 KB
-  int ns = 2;
-  ALayout L = a_layout(Z, T, mz, np, mode, ns);
-  if (L.total > per3) {
+  // one z-pencil per thread in phase 1: NP = AT / T planes per batch.  In order
+  // of preference (measured at c2 / c4): two stage buffers at three CTAs per SM
+  // (3 x (75 + 1 reserved) KB <= 228 KB), one buffer at two or more CTAs per SM,
+  // then half the planes per batch at three CTAs per SM (large Z*T planes such
+  // as c4's 128 x 32 backward, two input arrays, would otherwise leave one CTA
+  // per SM)
+  const int np0 = std::max(1, (AT + T - 1) / T);
+  const size_t per3 = 75 * 1024, per2 = 113 * 1024;
+  const int cand[4][2] = {{np0, 2}, {np0, 1}, {std::max(1, np0 / 2), 2}, {std::max(1, np0 / 2), 1}};
+  const size_t lim[4] = {per3, per2, per3, per3};
+  int np = np0, ns = 1;
+  ALayout L{};
+  bool found = false;
+  for (int i = 0; i < 4; ++i) {
+    const auto& c = cand[i];
+    L = a_layout(Z, T, mz, c[0], mode, c[1]);
+    if (L.total <= lim[i]) {
+      np = c[0];
+      ns = c[1];
+      found = true;
+      break;
+    }
+  }
+  if (!found) {   // fall back to one buffer, as many planes as fit one CTA
     ns = 1;
     L = a_layout(Z, T, mz, np, mode, ns);
-  }
-  while (np > 1 && L.total > 200 * 1024) {
-    --np;
-    L = a_layout(Z, T, mz, np, mode, ns);
+    while (np > 1 && L.total > 200 * 1024) {
+      --np;
+      L = a_layout(Z, T, mz, np, mode, ns);
+    }
   }
   *NP = np;
   *NS = ns;

@@ -2,6 +2,7 @@
 // unit per padded width CP): eligibility, shared-memory size, tensor map.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -26,6 +27,11 @@ bool pass_c3_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   if (LZ != 8 && LZ != 16 && LZ != 32) return false;
   const int tch = C3T / LZ;
   if (tch > T) return false;   // T % 4 != 0: cp.async tiles (TMA rows would be misaligned)
+  // long t codelets (LT >= 30) spill under the two-CTA register cap of the
+  // transform warps: measured slower than pass_c2 at c4 (LT = 32, TMA tiles);
+  // kept where pass_c2 has no TMA either (T % 4 != 0, c3: faster)
+  const int lt_needed = std::min(2 * mt - 1, T);
+  if (lt_needed > 16 && T % 4 == 0) return false;
   const size_t s = c3_layout(CP, C, Z, T, mz, mt, LZ).total;
   if (s > 227 * 1024) return false;
   *CPo = CP;
@@ -39,7 +45,8 @@ cudaError_t launch_pass_c3(const PassCParams& p0, int LZ, int LT, int CP, int gr
   p.TCH = C3T / LZ;
   C2Maps maps;
   std::memset(&maps, 0, sizeof maps);
-  p.use_tma = (p.T % 4 == 0 && c2_encode_tile_map(&maps.m[0], p.v, p, LZ)) ? 1 : 0;
+  // the TMA kernel assumes full t chunks; a ragged last chunk takes the cp.async kernel
+  p.use_tma = (p.T % 4 == 0 && p.T % p.TCH == 0 && c2_encode_tile_map(&maps.m[0], p.v, p, LZ)) ? 1 : 0;
   p.VW = (p.T % 2 == 0) ? 2 : 1;   // cp.async piece (floats) of the non-TMA path
   switch (CP) {
     case 4: return launch_pass_c3_cp4(maps, p, LZ, LT, grid, smem, st);

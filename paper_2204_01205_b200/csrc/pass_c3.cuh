@@ -106,7 +106,7 @@ __device__ __forceinline__ void group_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int LZ, int LT, int CP, bool HALF>
+template <int LZ, int LT, int CP, bool HALF, bool TMA>
 __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
   static_assert(CP % 4 == 0 && CP <= 32 && (CP + 15) / 16 * 16 <= 32, "CP must be a multiple of 4, at most 32");
   static_assert(C3T % LZ == 0 && C3T / LZ >= 4, "LZ must divide the 128 tile points, TCH >= 4");
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
       const int rz = ti / nch, tc = ti - rz * nch;
       int bb;
       const int xy = col_split(c_, &bb);
-      if (p.use_tma) {
+      if (TMA) {
         if (ttid == 0) {
           mbar_expect_tx(&bar[0], tile_bytes);
           tma_load_5d(X, &maps.m[0], tc * TCH, rz, 0, xy, bb * C, &bar[0]);
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         mbar_wait(&bempty[b], (use & 1u) ^ 1u);
         // ---- split the v tile into the K-major tf32 hi / lo operands --------
         if (k > 0) mbar_wait(&bmma[(k - 1) & 1], ((k - 1) >> 1) & 1u);   // MMA k-1 done reading A
-        if (p.use_tma) {
+        if (TMA) {
           mbar_wait(&bar[0], tphase);
           tphase ^= 1u;
         } else {
@@ -325,10 +325,10 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         }
         float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
         // ---- phase 2: inverse z (real output), items (c, tt) -> U[b] --------
-        const int tcw = min(TCH, T - t0);   // ragged chunk: columns tt >= tcw are never stored
+        const int tcw = TMA ? TCH : min(TCH, T - t0);   // ragged chunk (cp.async path): columns tt >= tcw are never stored
         for (int it = (p.ablate & 1) ? C * TCH : ttid; it < C * TCH; it += NTT) {
           const int c = it / TCH, tt = it - c * TCH;
-          if (tt >= tcw) continue;
+          if (!TMA && tt >= tcw) continue;
           float2 e[LZ];
 #pragma unroll
           for (int i = 0; i < LZ; ++i)
@@ -374,8 +374,8 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         const int pq = 32 * warp + 4 * (lane & 7);
         const int sq = pq / TCH, tq = pq - sq * TCH;
         const long long gq = cbase + (long long)(rz + p.Qz * sq) * T + t0 + tq;
-        const int nv = min(4, T - t0 - tq);   // valid points of this quad (ragged last chunk)
-        const bool v4 = (T % 4 == 0) && nv == 4;
+        const int nv = TMA ? 4 : min(4, T - t0 - tq);   // valid points of this quad (ragged last chunk)
+        const bool v4 = TMA || ((T % 4 == 0) && nv == 4);
 #pragma unroll
         for (int j = 0; j < (CP + 3) / 4; ++j) {
           const int o = (lane >> 3) + 4 * j;
@@ -414,7 +414,10 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
 template <int LZ, int LT, int CP>
 cudaError_t launch_c3_cp(const C2Maps& maps, const PassCParams& p, int grid, size_t smem, cudaStream_t st) {
   const bool half = 2 * p.mz == LZ;
-  void (*k)(C2Maps, PassCParams) = half ? pass_c3_fwd_kernel<LZ, LT, CP, true> : pass_c3_fwd_kernel<LZ, LT, CP, false>;
+  // TMA tiles (T % 4 == 0, full t chunks) or cp.async tiles (ragged chunks, scalar stores)
+  void (*k)(C2Maps, PassCParams) =
+      p.use_tma ? (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, true> : pass_c3_fwd_kernel<LZ, LT, CP, false, true>)
+                : (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, false> : pass_c3_fwd_kernel<LZ, LT, CP, false, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   k<<<grid, c3_threads(CP, LZ), smem, st>>>(maps, p);
