@@ -24,12 +24,16 @@ bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   if (tmax * LZ > C2T) tmax = (C2T / LZ) & ~3;
   const char* nxe = std::getenv("FNO_PASS_C_NX");
   const int force_nx = nxe ? std::atoi(nxe) : 0;
-  struct Opt { size_t budget; int nx; };
-  const Opt opts[] = {{75 * 1024, 1}, {113 * 1024, 2}, {227 * 1024, 2}, {227 * 1024, 1}};
+  // full: only the largest t chunk (a whole 128-point tile).  The backward keeps
+  // two buffers while two CTAs per SM fit at full tiles, else takes one buffer at
+  // full tiles (c4: 3.49 vs 5.03 ms/launch with two buffers at half tiles)
+  struct Opt { size_t budget; int nx; bool full; };
+  const Opt opts[] = {{75 * 1024, 1, false}, {113 * 1024, 2, true}, {113 * 1024, 1, true}, {113 * 1024, 2, false},
+                      {227 * 1024, 2, false}, {227 * 1024, 1, false}};
   for (const Opt& o : opts) {
     if (force_nx && o.nx != force_nx) continue;
-    if (o.nx == 1 && mode != EPI_FWD && !force_nx) continue;   // bwd keeps two buffers
-    for (int cand = tmax; cand >= 4; cand -= 4) {
+    if (o.nx == 1 && mode != EPI_FWD && !force_nx && !o.full) continue;   // bwd: one buffer only at full tiles
+    for (int cand = tmax; cand >= 4 && (!o.full || cand == tmax); cand -= 4) {
       const size_t s = c2_layout(CP, C, Z, T, mz, mt, LZ, cand, mode, o.nx).total;
       if (s <= o.budget) {
         *CPo = CP;
