@@ -305,14 +305,14 @@ def run_ours(args, rank, world, local_rank):
     value = units / (ms_step / 1e3)
 
     # ---- end to end: pinned host inputs -> device, step, result -> host -------
-    h_v = torch.empty(local, dtype=torch.float32, pin_memory=True)
-    h_dy = torch.empty(local, dtype=torch.float32, pin_memory=True)
-    h_v.copy_(v0.cpu())
-    h_dy.copy_(dy.cpu())
-    h_out = torch.empty((L, C * C + C), dtype=torch.float32, pin_memory=True)
     res = torch.empty((L, C * C + C), device=dev)
-
-    if net is not None:     # network: input a and target y in, the loss out
+    if net is None:         # layer stack: the field v and the cotangent dy in, dW / db out
+        h_v = torch.empty(local, dtype=torch.float32, pin_memory=True)
+        h_dy = torch.empty(local, dtype=torch.float32, pin_memory=True)
+        h_v.copy_(v0.cpu())
+        h_dy.copy_(dy.cpu())
+        h_out = torch.empty((L, C * C + C), dtype=torch.float32, pin_memory=True)
+    else:                   # network: input a and target y in, the loss out
         h_v = torch.empty(a_in.shape, dtype=torch.float32, pin_memory=True)
         h_dy = torch.empty(y_t.shape, dtype=torch.float32, pin_memory=True)
         h_v.copy_(a_in.cpu())

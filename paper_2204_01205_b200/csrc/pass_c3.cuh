@@ -25,6 +25,10 @@
 //                           issues the next tile's TMA and 3 x KP/8 UMMAs
 //                           (M128 x NP x K8) into TMEM; then, per TMEM lane
 //                           (= point), z = D row + U, GELU, float4 stores
+// v tiles arrive by one TMA 5-D tensor-map load when T % 4 == 0 and the t chunks
+// are full (kernel TMA = true), else by cp.async row pieces issued by the
+// transform warps (a z row of T floats is then not 16-byte aligned; the ragged
+// last t chunk is computed but not stored).
 // U and the TMEM accumulator are double-buffered with full / empty mbarriers
 // between the two groups.  (Measured alternatives, slower at c2: more v-tile
 // stages paid for by holding Bb for half the t range at a time -- DRAM line
