@@ -285,14 +285,19 @@ __global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
   }
 }
 
-// deterministic fixed-order (ascending row) column sums; columns [0, split)
-// go to out0, [split, len) to out1 (nullable)
+// deterministic fixed-order column sums; columns [0, split) go to out0,
+// [split, len) to out1 (nullable)
+// (one warp per column: lane i sums rows i, i + 32, ... in ascending order, then
+// a fixed butterfly -- the same order on every run and every rank)
 __global__ void rowsum_kernel(const float* __restrict__ parts, int nparts, int len, int split, float* out0, float* out1,
                               int accumulate) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (l >= len) return;
   float s = 0.f;
-  for (int p = 0; p < nparts; ++p) s += parts[(long long)p * len + l];
+  for (int p = lane; p < nparts; p += 32) s += parts[(long long)p * len + l];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane != 0) return;
   float* o = (l < split) ? out0 + l : (out1 ? out1 + (l - split) : nullptr);
   if (o) *o = accumulate ? *o + s : s;
 }
@@ -375,7 +380,7 @@ cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st) {
 
 cudaError_t launch_rowsum(const float* parts, int nparts, int len, int split, float* out0, float* out1, int accumulate,
                           cudaStream_t st) {
-  rowsum_kernel<<<(len + 127) / 128, 128, 0, st>>>(parts, nparts, len, split, out0, out1, accumulate);
+  rowsum_kernel<<<(len + 7) / 8, 256, 0, st>>>(parts, nparts, len, split, out0, out1, accumulate);
   return cudaGetLastError();
 }
 
