@@ -47,9 +47,15 @@ namespace fno {
 constexpr int C3T = 128;   // tile points = M = TMEM lanes = epilogue threads (warps 0-3)
 
 // transform threads: one phase-2 item (c, t) each when that fits in 4-5 warps
+#ifndef FNO_C3_EXTRA
+#define FNO_C3_EXTRA 32   // one more transform warp: the operand split and phase 1 spread wider (c2 fwd 0.664 -> 0.627 ms)
+#endif
 __host__ __device__ constexpr int c3_transform_threads(int CP, int LZ) {
-  return (CP * (C3T / LZ) + 31) / 32 * 32 > 160 ? 128
-         : ((CP * (C3T / LZ) + 31) / 32 * 32 < 128 ? 128 : (CP * (C3T / LZ) + 31) / 32 * 32);
+#ifdef FNO_C3_NTT
+  return FNO_C3_NTT;
+#endif
+  return FNO_C3_EXTRA + ((CP * (C3T / LZ) + 31) / 32 * 32 > 160 ? 128
+         : ((CP * (C3T / LZ) + 31) / 32 * 32 < 128 ? 128 : (CP * (C3T / LZ) + 31) / 32 * 32));
 }
 __host__ __device__ constexpr int c3_threads(int CP, int LZ) { return C3T + c3_transform_threads(CP, LZ); }
 
