@@ -54,6 +54,25 @@ std::once_flag g_encode_once;
 }  // namespace
 
 // (T, Qz, LZ, Xl*Yl, B*C) view of an NCXYZT field; box [C][1][LZ][1][TCH]
+// rows per TMA row group: G consecutive z rows of T floats make one row of the
+// view, so that every global stride is a multiple of 16 bytes even when
+// T % 4 != 0 (element (z = rz + Qz s, t) with rz = G a + r sits at inner
+// coordinate r T + t, group a, s).  A box must also start 16-byte aligned, so
+// the t chunks of a z row with (r T) % 4 = sh start sh points early: chunk tc
+// covers t in [tc TCH - sh, (tc + 1) TCH - sh), and the ceil(T / TCH) chunks
+// must still cover [0, T).  0: no TMA view exists (Qz % G != 0, chunks would
+// not cover, or a stride / the base is not 16-byte aligned).
+int c2_tile_group(const PassCParams& p, int LZ, const float* base) {
+  const int G = (p.T % 4 == 0) ? 1 : (p.T % 2 == 0 ? 2 : 4);
+  const long long ZT = (long long)p.Z * p.T;
+  if (p.Qz % G != 0 || p.TCH % 4 != 0 || p.TCH > 256 || LZ > 256 || p.C > 256) return 0;
+  if ((ZT * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return 0;
+  const int nch = (p.T + p.TCH - 1) / p.TCH;
+  for (int r = 0; r < G; ++r)
+    if (((r * p.T) & 3) + p.T > nch * p.TCH) return 0;
+  return G;
+}
+
 bool c2_encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, int LZ) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
@@ -63,10 +82,12 @@ bool c2_encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p,
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   });
   if (!g_encode) return false;
-  const cuuint64_t dims[5] = {cuuint64_t(p.T), cuuint64_t(p.Qz), cuuint64_t(LZ), cuuint64_t(p.Xl) * p.Yl,
+  const int G = c2_tile_group(p, LZ, base);
+  if (G == 0) return false;
+  const cuuint64_t dims[5] = {cuuint64_t(G) * p.T, cuuint64_t(p.Qz / G), cuuint64_t(LZ), cuuint64_t(p.Xl) * p.Yl,
                               cuuint64_t(p.B) * p.C};
   const cuuint64_t ZT = cuuint64_t(p.Z) * p.T;
-  const cuuint64_t strides[4] = {cuuint64_t(p.T) * 4, cuuint64_t(p.Qz) * p.T * 4, ZT * 4,
+  const cuuint64_t strides[4] = {cuuint64_t(G) * p.T * 4, cuuint64_t(p.Qz) * p.T * 4, ZT * 4,
                                  cuuint64_t(p.Xl) * p.Yl * ZT * 4};
   const cuuint32_t box[5] = {cuuint32_t(p.TCH), 1, cuuint32_t(LZ), 1, cuuint32_t(p.C)};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
@@ -82,8 +103,9 @@ cudaError_t launch_pass_c2(const PassCParams& p0, int LZ, int LT, int CP, int mo
   C2Maps maps;
   std::memset(&maps, 0, sizeof maps);
   p.use_tma = 0;
-  if (p.T % 4 == 0 && p.TCH <= 256 && LZ <= 256 && p.C <= 256) {
-    const float* src0 = mode == EPI_FWD ? p.v : p.dy;
+  const float* src0 = mode == EPI_FWD ? p.v : p.dy;
+  p.tma_g = c2_tile_group(p, LZ, src0);
+  if (p.tma_g > 0 && (mode == EPI_FWD || c2_tile_group(p, LZ, p.v) == p.tma_g)) {
     bool ok = c2_encode_tile_map(&maps.m[0], src0, p, LZ);
     if (ok && mode == EPI_BWD) ok = c2_encode_tile_map(&maps.m[1], p.v, p, LZ);
     p.use_tma = ok ? 1 : 0;

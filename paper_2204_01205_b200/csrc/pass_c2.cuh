@@ -77,6 +77,14 @@ __host__ __device__ inline C2Layout c2_layout(int CP, int C, int Z, int T, int m
   return L;
 }
 
+// points [k0, k1) of a quad, one scalar store each
+__device__ __forceinline__ void store_quad_part(float* dst, float4 r, int k0, int k1) {
+  if (k0 <= 0 && k1 > 0) dst[0] = r.x;
+  if (k0 <= 1 && k1 > 1) dst[1] = r.y;
+  if (k0 <= 2 && k1 > 2) dst[2] = r.z;
+  if (k0 <= 3 && k1 > 3) dst[3] = r.w;
+}
+
 __device__ __forceinline__ float4 f4fma(float w, float4 x, float4 a) {
   a.x = fmaf(w, x.x, a.x); a.y = fmaf(w, x.y, a.y); a.z = fmaf(w, x.z, a.z); a.w = fmaf(w, x.w, a.w);
   return a;
@@ -94,7 +102,9 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
 
 // HALF: mz = LZ / 2 (nk = LZ / 2 + 1 at compile time: the zero z-spectrum
 // inputs of the inverse z codelet fold away)
-template <int LZ, int LT, int CP, int EPI, bool HALF>
+// RAG: t chunks may be ragged or phase-shifted (T % TCH != 0, row-group TMA
+// view, or cp.async tiles); false compiles the full-chunk, aligned-quad case
+template <int LZ, int LT, int CP, int EPI, bool HALF, bool RAG>
 __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
   static_assert(CP % 4 == 0, "CP must be a multiple of 4");
   constexpr int NA = (EPI == EPI_FWD) ? 1 : 2;
@@ -189,7 +199,9 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
         const int xy = col_split(c_, &b);
         mbar_expect_tx(&bar[which], tile_bytes * NA);
 #pragma unroll
-        for (int a = 0; a < NA; ++a) tma_load_5d(dst + a * CP * XPS, &maps.m[a], t0, rz, 0, xy, b * C, &bar[which]);
+        for (int a = 0; a < NA; ++a)
+          tma_load_5d(dst + a * CP * XPS, &maps.m[a], (rz % p.tma_g) * T + t0 - (((rz % p.tma_g) * T) & 3),
+                      rz / p.tma_g, 0, xy, b * C, &bar[which]);
       }
       return;
     }
@@ -277,16 +289,30 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
 
     for (int ti = 0; ti < tpc; ++ti) {
       const int rz = ti / nch, tc = ti - rz * nch;
-      const int t0 = tc * TCH;
-      const int tcw = min(TCH, T - t0);
+      // TMA tiles of z rows with (z T) % 4 != 0 start sh points early (16-byte
+      // aligned rows, c2_tile_group); the tile's valid columns are [ta, tb)
+      const int sh = (RAG && tma && p.tma_g > 1) ? ((rz & (p.tma_g - 1)) * T) & 3 : 0;
+      const int t0 = tc * TCH - sh;
+      const int ta = RAG ? max(0, -t0) : 0, tb = RAG ? min(TCH, T - t0) : TCH, tcw = tb - ta;
       if (NX == 2) {
         if (ti + 1 < tpc) issue_tile(col, ti + 1, buf ^ 1);
         else if (col_next < p.n_cols) issue_tile(col_next, 0, buf ^ 1);
       }
       float* X = reinterpret_cast<float*>(smem_raw + (buf ? L.x1 : L.x0));
       if (tma) {
-        mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);   // this tile's inputs (OOB t zero-filled)
+        mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);   // this tile's inputs
         phase_bits ^= 1u << buf;
+        if (EPI == EPI_BWD && RAG && tcw < TCH) {   // ragged t chunk (t outside [0, T): other rows or OOB): exact zeros for dW / db
+          const int w = TCH - tcw;
+          for (int e = tid; e < 2 * C * LZ * w; e += C2T) {
+            const int a = e / (C * LZ * w), r = e - a * (C * LZ * w);
+            const int row = r / w, j = r - row * w;
+            const int tt = j < ta ? j : tcw + j;
+            X[a * CP * XPS + row * TCH + tt] = 0.f;
+          }
+          fence_proxy_async();   // generic stores before the next TMA write of this buffer
+          __syncthreads();
+        }
       } else {
         if (NX == 2) {
           cp_commit();
@@ -295,7 +321,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
           cp_wait<0>();
         }
         __syncthreads();
-        if (EPI == EPI_BWD && tcw < TCH) {   // ragged t chunk: exact zeros for dW / db
+        if (EPI == EPI_BWD && RAG && tcw < TCH) {   // ragged t chunk: exact zeros for dW / db
           const int w = TCH - tcw;
           for (int e = tid; e < 2 * C * LZ * w; e += C2T) {
             const int a = e / (C * LZ * w), r = e - a * (C * LZ * w);
@@ -307,7 +333,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
       }
       // ---- phase 2: inverse z (real output), items (c, tt) -> U ----------
       for (int it = (p.ablate & 1) ? C * tcw : tid; it < C * tcw; it += C2T) {
-        const int c = it / tcw, tt = it - c * tcw;
+        const int c = it / tcw, tt = ta + (it - c * tcw);
         float2 e[LZ];
 #pragma unroll
         for (int i = 0; i < LZ; ++i)
@@ -372,9 +398,11 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
         if (!tma) cp_commit();
       }
       // ---- epilogue: + u (+ b, GELU), stores -------------------------------
-      if (item1 && tq1 < tcw && !(p.ablate & 4)) {
+      const int k0 = RAG ? max(0, ta - tq1) : 0, k1 = RAG ? min(4, tb - tq1) : 4;   // valid points of this thread's quad
+      if (item1 && k0 < k1 && !(p.ablate & 4)) {
         const long long gs = cbase + rz * T + t0 + go1;
-        const int nv = min(4, tcw - tq1);
+        // TMA tiles start 16-byte aligned in memory (c2_tile_group), so do their full quads
+        const bool full4 = !RAG || ((vec_out || tma) && k0 == 0 && k1 == 4);
 #pragma unroll
         for (int j = 0; j < Q4; ++j) {
           const int o = qtr1 * Q4 + j;
@@ -387,25 +415,15 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
             r.x += bo; r.y += bo; r.z += bo; r.w += bo;
             if (p.zsave) {
               float* zo = p.zsave + gs + o * chan_stride;
-              if (vec_out && nv == 4) __stcs(reinterpret_cast<float4*>(zo), r);
-              else {
-                zo[0] = r.x;
-                if (nv > 1) zo[1] = r.y;
-                if (nv > 2) zo[2] = r.z;
-                if (nv > 3) zo[3] = r.w;
-              }
+              if (full4) __stcs(reinterpret_cast<float4*>(zo), r);
+              else store_quad_part(zo, r, k0, k1);
             }
             if (p.act_gelu) {
               r.x = gelu_f(r.x); r.y = gelu_f(r.y); r.z = gelu_f(r.z); r.w = gelu_f(r.w);
             }
           }
-          if (vec_out && nv == 4) __stcs(reinterpret_cast<float4*>(out), r);
-          else {
-            out[0] = r.x;
-            if (nv > 1) out[1] = r.y;
-            if (nv > 2) out[2] = r.z;
-            if (nv > 3) out[3] = r.w;
-          }
+          if (full4) __stcs(reinterpret_cast<float4*>(out), r);
+          else store_quad_part(out, r, k0, k1);
         }
       }
       __syncthreads();   // U and X[buf] free for reuse (and Bb after the last tile)
@@ -440,9 +458,12 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
 template <int LZ, int LT, int CP>
 cudaError_t launch_c2_cp(const C2Maps& maps, const PassCParams& p, int mode, int grid, size_t smem, cudaStream_t st) {
   const bool half = 2 * p.mz == LZ;
+  const bool rag = !p.use_tma || p.tma_g != 1 || p.T % p.TCH != 0 || p.T % 4 != 0;
   void (*k)(C2Maps, PassCParams) =
-      mode == EPI_FWD ? (half ? pass_c2_kernel<LZ, LT, CP, EPI_FWD, true> : pass_c2_kernel<LZ, LT, CP, EPI_FWD, false>)
-                      : (half ? pass_c2_kernel<LZ, LT, CP, EPI_BWD, true> : pass_c2_kernel<LZ, LT, CP, EPI_BWD, false>);
+      rag ? (mode == EPI_FWD ? (half ? pass_c2_kernel<LZ, LT, CP, EPI_FWD, true, true> : pass_c2_kernel<LZ, LT, CP, EPI_FWD, false, true>)
+                             : (half ? pass_c2_kernel<LZ, LT, CP, EPI_BWD, true, true> : pass_c2_kernel<LZ, LT, CP, EPI_BWD, false, true>))
+          : (mode == EPI_FWD ? (half ? pass_c2_kernel<LZ, LT, CP, EPI_FWD, true, false> : pass_c2_kernel<LZ, LT, CP, EPI_FWD, false, false>)
+                             : (half ? pass_c2_kernel<LZ, LT, CP, EPI_BWD, true, false> : pass_c2_kernel<LZ, LT, CP, EPI_BWD, false, false>));
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   k<<<grid, C2T, smem, st>>>(maps, p);
@@ -452,6 +473,7 @@ cudaError_t launch_c2_cp(const C2Maps& maps, const PassCParams& p, int mode, int
 // TMA tensor map of a tile input: (T, Qz, LZ, Xl*Yl, B*C) view of an NCXYZT
 // field, box [C][1][LZ][1][p.TCH] (pass_c2.cu)
 bool c2_encode_tile_map(CUtensorMap* m, const float* base, const PassCParams& p, int LZ);
+int c2_tile_group(const PassCParams& p, int LZ, const float* base);
 
 // per-width entry points (one translation unit per CP: pass_c2_cp<CP>.cu)
 cudaError_t launch_pass_c2_cp4(const C2Maps& maps, const PassCParams& p, int LZ, int LT, int mode, int grid, size_t smem,

@@ -46,7 +46,8 @@ cudaError_t launch_pass_c3(const PassCParams& p0, int LZ, int LT, int CP, int gr
   C2Maps maps;
   std::memset(&maps, 0, sizeof maps);
   // the TMA kernel assumes full t chunks; a ragged last chunk takes the cp.async kernel
-  p.use_tma = (p.T % 4 == 0 && p.T % p.TCH == 0 && c2_encode_tile_map(&maps.m[0], p.v, p, LZ)) ? 1 : 0;
+  p.tma_g = c2_tile_group(p, LZ, p.v);
+  p.use_tma = (p.tma_g > 0 && c2_encode_tile_map(&maps.m[0], p.v, p, LZ)) ? 1 : 0;
   p.VW = (p.T % 2 == 0) ? 2 : 1;   // cp.async piece (floats) of the non-TMA path
   switch (CP) {
     case 4: return launch_pass_c3_cp4(maps, p, LZ, LT, grid, smem, st);

@@ -25,10 +25,11 @@
 //                           issues the next tile's TMA and 3 x KP/8 UMMAs
 //                           (M128 x NP x K8) into TMEM; then, per TMEM lane
 //                           (= point), z = D row + U, GELU, float4 stores
-// v tiles arrive by one TMA 5-D tensor-map load when T % 4 == 0 and the t chunks
-// are full (kernel TMA = true), else by cp.async row pieces issued by the
-// transform warps (a z row of T floats is then not 16-byte aligned; the ragged
-// last t chunk is computed but not stored).
+// v tiles arrive by one TMA 5-D tensor-map load (kernel TMA = true; when
+// T % 4 != 0 the view's rows are groups of G = 2 or 4 z rows, so its strides
+// stay 16-byte multiples -- c2_tile_group), else by cp.async row pieces issued
+// by the transform warps.  The columns t >= T of a ragged last t chunk (the
+// next row of the group, or TMA zero fill) are computed but never stored.
 // U and the TMEM accumulator are double-buffered with full / empty mbarriers
 // between the two groups.  (Measured alternatives, slower at c2: more v-tile
 // stages paid for by holding Bb for half the t range at a time -- DRAM line
@@ -116,7 +117,9 @@ __device__ __forceinline__ void group_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int LZ, int LT, int CP, bool HALF, bool TMA>
+// RAG: t chunks may be ragged or phase-shifted (T % TCH != 0, row-group TMA
+// view, or cp.async tiles); false compiles the full-chunk, aligned-quad case
+template <int LZ, int LT, int CP, bool HALF, bool TMA, bool RAG>
 __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
   static_assert(CP % 4 == 0 && CP <= 32 && (CP + 15) / 16 * 16 <= 32, "CP must be a multiple of 4, at most 32");
   static_assert(C3T % LZ == 0 && C3T / LZ >= 4, "LZ must divide the 128 tile points, TCH >= 4");
@@ -217,10 +220,10 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
       const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
       return p.in + p.slab.off[dm.x] + ((c_ * C + c) * nkz + dm.y) * mt;
     };
-    // v tile (rz, t chunk tc) of column c_ into X: one TMA (thread 0) when T % 4
-    // == 0, else cp.async row pieces by all transform threads (a z row of T
-    // floats is not 16-byte aligned; the ragged chunk leaves stale columns that
-    // are never stored)
+    // v tile (rz, t chunk tc) of column c_ into X: one TMA (thread 0) on the
+    // row-group view (rz = G a + r -> inner coordinate r T + t0, group a), else
+    // cp.async row pieces by all transform threads; the ragged chunk leaves
+    // stale columns that are never stored
     auto issue_tile = [&](long long c_, int ti) {   // all transform threads
       const int rz = ti / nch, tc = ti - rz * nch;
       int bb;
@@ -228,7 +231,8 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
       if (TMA) {
         if (ttid == 0) {
           mbar_expect_tx(&bar[0], tile_bytes);
-          tma_load_5d(X, &maps.m[0], tc * TCH, rz, 0, xy, bb * C, &bar[0]);
+          const int r = (rz % p.tma_g) * T;   // 16-byte aligned start: the chunk begins (r & 3) points early
+          tma_load_5d(X, &maps.m[0], r + tc * TCH - (r & 3), rz / p.tma_g, 0, xy, bb * C, &bar[0]);
         }
         return;
       }
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
           asm volatile("prefetch.global.L1 [%0];" ::"l"(slab_at(col_next, r / (2 * mz), r % (2 * mz))));
       for (int ti = 0; ti < tpc; ++ti, ++k) {
         const int rz = ti / nch, tc = ti - rz * nch;
-        const int t0 = tc * TCH;
+        const int t0 = tc * TCH - ((RAG && TMA && p.tma_g > 1) ? ((rz & (p.tma_g - 1)) * T) & 3 : 0);   // first t of the tile
         const int b = k & 1;
         const unsigned use = k >> 1;
         // U[b] and TMEM D[b] drained by the epilogue (tile k - 2)
@@ -335,10 +339,10 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         }
         float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
         // ---- phase 2: inverse z (real output), items (c, tt) -> U[b] --------
-        const int tcw = TMA ? TCH : min(TCH, T - t0);   // ragged chunk (cp.async path): columns tt >= tcw are never stored
+        const int ta = RAG ? max(0, -t0) : 0, tb = RAG ? min(TCH, T - t0) : TCH;   // valid columns; the others are never stored
         for (int it = (p.ablate & 1) ? C * TCH : ttid; it < C * TCH; it += NTT) {
           const int c = it / TCH, tt = it - c * TCH;
-          if (!TMA && tt >= tcw) continue;
+          if (tt < ta || tt >= tb) continue;
           float2 e[LZ];
 #pragma unroll
           for (int i = 0; i < LZ; ++i)
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
       const long long cbase = (long long)bcol * C * chan_stride + (long long)xycol * ZT;
       for (int ti = 0; ti < tpc; ++ti, ++k) {
         const int rz = ti / nch, tc = ti - rz * nch;
-        const int t0 = tc * TCH;
+        const int t0 = tc * TCH - ((RAG && TMA && p.tma_g > 1) ? ((rz & (p.tma_g - 1)) * T) & 3 : 0);
         const int b = k & 1;
         const unsigned use = k >> 1;
         float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
@@ -384,12 +388,13 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         const int pq = 32 * warp + 4 * (lane & 7);
         const int sq = pq / TCH, tq = pq - sq * TCH;
         const long long gq = cbase + (long long)(rz + p.Qz * sq) * T + t0 + tq;
-        const int nv = TMA ? 4 : min(4, T - t0 - tq);   // valid points of this quad (ragged last chunk)
-        const bool v4 = TMA || ((T % 4 == 0) && nv == 4);
+        // valid points [k0, k1) of this quad (ragged chunks); TMA tiles are 16-byte aligned
+        const int k0 = RAG ? max(0, -(t0 + tq)) : 0, k1 = RAG ? min(4, T - t0 - tq) : 4;
+        const bool v4 = !RAG || ((TMA || T % 4 == 0) && k0 == 0 && k1 == 4);
 #pragma unroll
         for (int j = 0; j < (CP + 3) / 4; ++j) {
           const int o = (lane >> 3) + 4 * j;
-          if (o >= C || (p.ablate & 4) || nv <= 0) break;
+          if (o >= C || (p.ablate & 4) || k0 >= k1) break;
           float4 r = *reinterpret_cast<const float4*>(U + o * UPS + pq);
           const long long g = gq + o * chan_stride;
           if (v4) {
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
             const float rv[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              if (kk < nv) {
+              if (kk >= k0 && kk < k1) {
                 if (p.zsave) p.zsave[g + kk] = rv[kk];
                 p.out[g + kk] = p.act_gelu ? gelu_f(rv[kk]) : rv[kk];
               }
@@ -424,10 +429,12 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
 template <int LZ, int LT, int CP>
 cudaError_t launch_c3_cp(const C2Maps& maps, const PassCParams& p, int grid, size_t smem, cudaStream_t st) {
   const bool half = 2 * p.mz == LZ;
-  // TMA tiles (T % 4 == 0, full t chunks) or cp.async tiles (ragged chunks, scalar stores)
+  const bool rag = p.tma_g != 1 || p.T % (C3T / LZ) != 0 || p.T % 4 != 0;
+  // TMA tiles (any row-group view, c2_tile_group) or cp.async tiles
   void (*k)(C2Maps, PassCParams) =
-      p.use_tma ? (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, true> : pass_c3_fwd_kernel<LZ, LT, CP, false, true>)
-                : (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, false> : pass_c3_fwd_kernel<LZ, LT, CP, false, false>);
+      !p.use_tma ? (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, false, true> : pass_c3_fwd_kernel<LZ, LT, CP, false, false, true>)
+      : rag      ? (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, true, true> : pass_c3_fwd_kernel<LZ, LT, CP, false, true, true>)
+                 : (half ? pass_c3_fwd_kernel<LZ, LT, CP, true, true, false> : pass_c3_fwd_kernel<LZ, LT, CP, false, true, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   k<<<grid, c3_threads(CP, LZ), smem, st>>>(maps, p);
