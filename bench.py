@@ -1,20 +1,25 @@
 #!/usr/bin/env python
 """bench.py — throughput of the 4D FNO spectral-layer hot path (arXiv 2204.01205).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4|c5]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
 
 A step is one training pass of the whole hot path over
 one synthetic batch: the forward of `layers` DFNO blocks in training mode
-(storing z and V^), then their backward (dv, dR, dW, db), on the BASELINE.json
-configs[1] shape (4D Navier-Stokes-shaped: 64x64x64x32 per GPU, width 20,
-modes 8, 4 Fourier layers, batch 1).  Multi-GPU runs are weak-scaled exactly
-like the paper's App. A spatial study: the per-GPU box stays
-64x64x64x32 and the global grid grows over an x/y process grid
-(1,1) (2,1) (2,2) (4,2), with the pencil all-to-all over NCCL/NVLink.
+(storing z and V^), then their backward (dv, dR, dW, db).  Default workload:
+BASELINE.json configs[2] (c3), the shape the metric "fwd+bwd at 1/2/4/8 B200"
+is quoted on: the CO2-multiphase-shaped training step,
+global grid 64x64x64x30, width 20, modes 12, 4 Fourier layers, batch 1,
+strong-scaled over the x/y process grids (1,1) (2,1) (2,2) (4,2),
+with the pencil repartitions over NVLink.  --config c2 | c4 (weak, per-GPU box
+fixed) | c5 select the other BASELINE configs.
 
 metric: grid-points x channels x layers processed (fwd+bwd) per second, whole
-job; value = B * X*Y*Z*T (global) * C * layers / step time (max over ranks).
+job; value = B * X*Y*Z*T (global) * C * layers / step time, the step time the
+median over K repetitions (each bracketed by a barrier, device-timed with CUDA
+events, max over ranks).  The line also carries the per-phase times (forward
+inference, forward training, backward), the whole-step HBM /
+NVLink roofline of SURVEY §8(d) and the dominant kernel's roofline.
 """
 
 from __future__ import annotations
@@ -32,19 +37,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "4D FNO layer grid-pts·ch/s fwd+bwd at 1/2/4/8 B200; % HBM/NVLink roofline"
 PGRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
-CONFIG_INDEX = 2            # BASELINE.json configs[1] (c2); --config selects another
+CONFIG_INDEX = 3            # BASELINE.json configs[2] (c3, the metric's shape); --config selects another
 STRONG = {"c3", "c5"}       # strong-scaled configs: the global grid is fixed (BASELINE.json)
 WORKLOADS = {
     "c2": "c2: 4D Navier-Stokes-shaped DFNO training step (fwd+bwd), 64x64x64x32 per GPU, width 20, modes 8, "
           "4 Fourier layers, batch 1 (BASELINE.json configs[1])",
     "c3": "c3: CO2-multiphase-shaped DFNO training step (fwd+bwd), global 64x64x64x30, width 20, modes 12, "
-          "4 Fourier layers, batch 1, x/y-decomposed (strong scaling; BASELINE.json configs[2])",
+          "4 Fourier layers, batch 1, x/y-decomposed over (1,1)/(2,1)/(2,2)/(4,2) (strong scaling; "
+          "BASELINE.json configs[2], the configuration the metric is quoted on)",
     "c4": "c4: weak-scaling 4D FNO, 64x128x128x32 per GPU, width 20, modes 12, 4 Fourier layers, fwd+bwd, batch 1 "
           "(BASELINE.json configs[3])",
     "c5": "c5: largest one-box instance, global 256x256x256x32, width 20, modes 16, 4 Fourier layers, fwd+bwd, "
           "batch 1 (BASELINE.json configs[4])",
 }
-REF_WIDTH = 4               # oracle sample: channels per reference step
+REF_XY_DIV = 4              # oracle sample: x/y sub-box (1/16 of the per-GPU points) at full width
 
 
 def _env_int(k, d):
@@ -181,6 +187,108 @@ def load_traffic(config):
     return {}
 
 
+def step_roofline(grid, local, modes, C, B, L, P, hbm_gbs, a2a):
+    """SURVEY §8(d) roofline of one training step per GPU: algorithmic bytes
+    per point-channel (fp32 field, complex64 spectra; r = 2mz mt / (Z T) the
+    slab fraction, rho = M / N the retained-mode fraction)
+        fwd (inference) 12 + 32 r + 8 C rho      fwd (training) + 4 + 8 rho
+        bwd             24 + 32 r + 16 C rho + 8 rho
+    on HBM, plus 2 x 8 r (P-1)/P per layer pass on NVLink; t_roof = HBM bytes /
+    BW_HBM + NVLink bytes / BW_NVL (sum: the stages are a dependency chain)
+    and the max() form.  BW_NVL: the NCCL all-to-all measured here at the
+    exchange message size (N > 1), 900 GB/s nominal for context."""
+    X, Y, Z, T = grid
+    mx, my, mz, mt = modes
+    r = 2.0 * mz * mt / (Z * T)
+    rho = 8.0 * mx * my * mz * mt / float(X * Y * Z * T)
+    n_loc = B * C * local[2] * local[3] * local[4] * local[5]
+    per = {"fwd_inference": 12 + 32 * r + 8 * C * rho,
+           "fwd_train": 12 + 32 * r + 8 * C * rho + 4 + 8 * rho,
+           "bwd": 24 + 32 * r + 16 * C * rho + 8 * rho}
+    nvl_pass = 2 * 8 * r * (P - 1) / P
+    if P > 1 and a2a:
+        nvl_gbs, nvl_kind = a2a["GBps_per_gpu"], "measured NCCL all-to-all at the exchange message size"
+    else:
+        nvl_gbs, nvl_kind = 900.0, "nominal (no exchange at P = 1)" if P == 1 else "nominal"
+
+    def t(hbm_b, nvl_b):
+        th = hbm_b / (hbm_gbs * 1e9) * 1e3
+        tn = nvl_b / (nvl_gbs * 1e9) * 1e3 if nvl_b else 0.0
+        return th, tn
+
+    out = {"bytes_per_pt_ch_per_layer": {k: round(v, 3) for k, v in per.items()},
+           "nvl_bytes_per_pt_ch_per_layer_pass": round(nvl_pass, 4),
+           "bw_hbm_gbs": hbm_gbs, "bw_hbm_nominal_gbs": 8000.0, "bw_nvl_gbs": round(nvl_gbs, 1),
+           "bw_nvl_kind": nvl_kind, "bw_nvl_nominal_gbs": 900.0, "phases": {}}
+    for name, b in per.items():
+        th, tn = t(b * n_loc * L, nvl_pass * n_loc * L)
+        out["phases"][name] = {"t_roof_sum_ms": round(th + tn, 4), "t_roof_max_ms": round(max(th, tn), 4)}
+    hbm_step = (per["fwd_train"] + per["bwd"]) * n_loc * L
+    nvl_step = 2 * nvl_pass * n_loc * L
+    th, tn = t(hbm_step, nvl_step)
+    out.update({"hbm_bytes": int(hbm_step), "nvl_bytes": int(nvl_step), "t_hbm_ms": round(th, 4),
+                "t_nvl_ms": round(tn, 4), "t_roof_sum_ms": round(th + tn, 4), "t_roof_max_ms": round(max(th, tn), 4)})
+    return out
+
+
+def measure_all_to_all(per_peer_bytes, world, dev, timed):
+    """NCCL all-to-all (torch.distributed, the same NVLink fabric the plan's
+    communicator uses) with `per_peer_bytes` to every peer: GB/s each GPU sends."""
+    import torch
+    import torch.distributed as dist
+    n = max(1, per_peer_bytes // 4)
+    src = torch.ones(n * world, dtype=torch.float32, device=dev)
+    dst = torch.empty_like(src)
+    for _ in range(3):
+        dist.all_to_all_single(dst, src)
+    ms = statistics.median(timed(lambda: dist.all_to_all_single(dst, src), 10))
+    sent = 4 * n * (world - 1)
+    return {"per_peer_bytes": int(4 * n), "ms": round(ms, 4), "GBps_per_gpu": round(sent / (ms / 1e3) / 1e9, 1)}
+
+
+def plan_kernels(plan):
+    """Which pass C kernel family the plan selected per epilogue."""
+    try:
+        import paper_2204_01205_b200 as fno
+        return fno.plan_pass_c_kernels(plan)
+    except Exception:
+        return None
+
+
+def torch_cpu_context(local, modes, C, reps=1):
+    """Context only: the same DFNO block, fwd + bwd by
+    autograd, written with torch CPU fp32 rFFTs on all host cores -- the
+    like-for-like of the paper's CPU inference (PyTorch on EPYC).
+    Not the oracle, not the product path."""
+    import torch
+    X, Y, Z, T = local[2:]
+    mx, my, mz, mt = modes
+    g = torch.Generator().manual_seed(5)
+    v = torch.randn((1, C, X, Y, Z, T), generator=g, requires_grad=True)
+    R = torch.randn((C, C, 2 * mx, 2 * my, 2 * mz, mt), dtype=torch.complex64, generator=g, requires_grad=True)
+    W = torch.randn((C, C), generator=g, requires_grad=True)
+    kx = torch.cat([torch.arange(mx), torch.arange(X - mx, X)])
+    ky = torch.cat([torch.arange(my), torch.arange(Y - my, Y)])
+    kz = torch.cat([torch.arange(mz), torch.arange(Z - mz, Z)])
+
+    def layer(v):
+        f = torch.fft.rfftn(v, dim=(2, 3, 4, 5))[:, :, kx][:, :, :, ky][:, :, :, :, kz][..., :mt]
+        w = torch.einsum("bixyzt,ioxyzt->boxyzt", f, R)
+        full = torch.zeros((1, C, X, Y, Z, T // 2 + 1), dtype=torch.complex64)
+        full[:, :, kx[:, None, None], ky[None, :, None], kz[None, None, :], :mt] = w
+        u = torch.fft.irfftn(full, s=(X, Y, Z, T), dim=(2, 3, 4, 5))
+        return torch.nn.functional.gelu(torch.einsum("oi,bixyzt->boxyzt", W, v) + u)
+
+    layer(v).sum().backward()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        layer(v).sum().backward()
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(v.numel() / dt, 1), "unit": "grid-pts·ch/s", "threads": torch.get_num_threads(),
+            "kind": "torch CPU fp32 rFFT layer fwd+bwd (autograd), context only",
+            "sample": f"one block on the per-GPU grid {list(local[2:])}, width {C}; {dt:.2f} s"}
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -258,35 +366,88 @@ def run_ours(args, rank, world, local_rank):
         step()
     barrier()
 
-    # ---- the step as one CUDA graph (layer stack; the network's Adam step
-    # count lives on the host, so that mode stays eager) --------------------
+    # ---- each timed callable as one CUDA graph (layer stack; the network's
+    # Adam step count lives on the host, so that mode stays eager) ------------
     use_graph = not args.no_graph and net is None
-    run = step
-    per_step = None
-    if use_graph:
-        graph = torch.cuda.CUDAGraph()
-        n_c = fno.kernel_launches()
-        with torch.cuda.graph(graph):
-            step()
-        per_step = fno.kernel_launches() - n_c
-        graph.replay()
-        barrier()
-        run = graph.replay
+    graphs = []
 
-    # ---- timed region (device clock, CUDA events on the launching stream) ----
+    def as_graph(fn):
+        if not use_graph:
+            return fn, None
+        g_ = torch.cuda.CUDAGraph()
+        n_c = fno.kernel_launches()
+        with torch.cuda.graph(g_):
+            fn()
+        per = fno.kernel_launches() - n_c
+        g_.replay()
+        barrier()
+        graphs.append(g_)
+        return g_.replay, per
+
+    run, per_step = as_graph(step)
+
+    def timed(fn, reps):
+        """Per-repetition device times (ms): a barrier before each repetition,
+        CUDA events on the launching stream, then the max over ranks."""
+        ts = []
+        for _ in range(reps):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        t = torch.tensor(ts, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.tolist()]
+
+    # ---- timed region: K repetitions of the step ------------------------------
     n0 = fno.kernel_launches()
     sampler = ClockSampler([nvml_index(local_rank)])
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
-        barrier()
-        start.record(stream)
-        for _ in range(args.steps):
-            run()
-        end.record(stream)
-        end.synchronize()
+        step_ms = timed(run, args.steps)
         barrier()
     launches = per_step * args.steps if use_graph else fno.kernel_launches() - n0
-    ms = start.elapsed_time(end)
+    ms_step = float(statistics.median(step_ms))
+    ms_mean = float(statistics.fmean(step_ms))
+    units = B * grid[0] * grid[1] * grid[2] * grid[3] * C * L
+    value = units / (ms_step / 1e3)
+
+    # ---- phases (PAPER.md:234: inference forward, training forward, backward) --
+    phases = None
+    if net is None and not args.no_phases:
+        ys = [torch.empty_like(v0) for _ in range(L)]
+
+        def fwd_infer():
+            x = acts[0]
+            for l in range(L):
+                fno.layer_fwd(plan, x, Rs[l], Ws[l], bs[l], ys[l])
+                x = ys[l]
+
+        def fwd_train():
+            for l in range(L):
+                fno.layer_fwd(plan, acts[l], Rs[l], Ws[l], bs[l], acts[l + 1], zs[l], vhs[l])
+
+        def bwd_only():
+            cur = 0
+            for l in reversed(range(L)):
+                nxt = 1 if cur != 1 else 2
+                fno.layer_bwd(plan, acts[l], zs[l], vhs[l], g[cur], Rs[l], Ws[l], g[nxt], dR[l], dW[l], db[l])
+                cur = nxt
+
+        phases = {}
+        nrep = max(5, min(args.steps, 20))
+        for name, fn in (("fwd_inference", fwd_infer), ("fwd_train", fwd_train), ("bwd", bwd_only)):
+            fn()
+            barrier()
+            r_, _ = as_graph(fn)
+            ms_ = float(statistics.median(timed(r_, nrep)))
+            phases[name] = {"ms": round(ms_, 4), "value": round(units / (ms_ / 1e3), 1),
+                            "ms_per_layer": round(ms_ / L, 4)}
+        del ys
+
     # per-stage CUDA events (library profiling hooks) on separate eager steps
     nprof = max(2, min(args.steps, 5))
     plan.profile_enable(True)
@@ -296,14 +457,13 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     prof = plan.profile_read()
     plan.profile_enable(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
-    ms_step = ms_total / args.steps
-    units = B * grid[0] * grid[1] * grid[2] * grid[3] * C * L
-    value = units / (ms_step / 1e3)
 
+    # NCCL all-to-all bandwidth at this config's exchange message size (BW_NVL of
+    # the SURVEY §8(d) roofline): bytes each GPU sends / device time, median
+    a2a = None
+    if world > 1:
+        per_peer = 8 * B * C * local[2] * local[3] * max(kz_hi - kz_lo, 1) * modes[3]
+        a2a = measure_all_to_all(per_peer, world, dev, timed)
     # ---- end to end: pinned host inputs -> device, step, result -> host -------
     res = torch.empty((L, C * C + C), device=dev)
     if net is None:         # layer stack: the field v and the cotangent dy in, dW / db out
@@ -406,15 +566,28 @@ def run_ours(args, rank, world, local_rank):
                   "GBps": (round(sb[k] / (v[0] / v[1] / 1e3) / 1e9, 1) if k in sb else None)}
               for k, v in sorted(prof.items())}
 
-    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ---
+    # ---- whole-step roofline (algorithmic HBM + NVLink bytes) ---
+    step_roof = step_roofline(grid, local, modes, C, B, L, world, peak, a2a)
+    step_roof["t_measured_ms"] = round(ms_step, 4)
+    step_roof["frac_sum"] = round(step_roof["t_roof_sum_ms"] / ms_step, 4)
+    step_roof["frac_max"] = round(step_roof["t_roof_max_ms"] / ms_step, 4)
+    if phases:
+        for name, ph in phases.items():
+            ph["t_roof_ms"] = step_roof["phases"][name]["t_roof_sum_ms"]
+            ph["frac"] = round(ph["t_roof_ms"] / ph["ms"], 4)
+
+    # ---- CPU baselines: the oracle on a bounded sample (rank 0, N=1 only) -----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and net is None:
         cpu = oracle_sample(args, v0.detach().cpu().numpy(), dy.detach().cpu().numpy(), modes, repeats=1)
+        cpu["context_torch_cpu"] = torch_cpu_context(local, modes, C)
 
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "grid-pts·ch/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "ms_per_step_mean": round(ms_mean, 4), "timing": "median of K repetitions, a barrier before each, "
+                                                          "CUDA events, max over ranks",
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": f"synthetic (seeded {'CO2' if cfg['shape'] == 'co2' else 'NS'}-shaped fields, random-init weights)",
         "config": {"workload": (WORKLOADS[cfg["name"]] if net is None else
@@ -425,7 +598,9 @@ def run_ours(args, rank, world, local_rank):
                    "layers": L, "parallelism": f"x/y domain decomposition {px}x{py}",
                    "launch": "one CUDA graph per step (replayed)" if use_graph else "eager",
                    "l2": f"inputs larger than L2 ({B * C * int(np.prod(local[2:])) * 4 / 1e6:.0f} MB field per "
-                         f"layer per GPU; L2 126 MB)"},
+                         f"layer per GPU; L2 126 MB)",
+                   "env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("FNO_")},
+                   "pass_c": plan_kernels(plan)},
         "e2e": {"value": round(e2e_value, 1), "unit": "grid-pts·ch/s", "ms_per_step": round(e2e_ms, 4),
                 "overlap": ("the next step's pinned-host inputs are copied on a second stream while the current step "
                             "computes (two device input slots)" if net is None else "none"),
@@ -433,16 +608,20 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(h_out.numel() * 4)},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "step_roofline": step_roof,
+        "phases": phases,
+        "nccl_all_to_all": a2a,
         "stages": stages,
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if use_graph:
+    if graphs:
         torch.cuda.synchronize()
-        graph.reset()          # release the captured NCCL / peer-exchange work before the communicator
-        del graph
+        for g_ in graphs:      # release the captured NCCL / peer-exchange work before the communicator
+            g_.reset()
+        graphs.clear()
     if world > 1:
         dist.barrier()
     plan.destroy()
@@ -450,17 +629,29 @@ def run_ours(args, rank, world, local_rank):
         comm.destroy()
 
 
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        return {"blas": [(d.get("internal_api"), d.get("num_threads")) for d in info]}
+    except Exception as e:       # noqa: BLE001
+        return {"blas": f"unknown ({e})"}
+
+
 def oracle_sample(args, v, dy, modes, repeats=1):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
-    one DFNO block forward + backward on the full per-GPU grid, REF_WIDTH of
-    the 20 channels.  Returns the cpu_baseline object (grid-pts·ch/s)."""
+    one DFNO block forward + backward (oracle.spectral.layer_fwd + layer_bwd) at
+    the full width of the config, on an x/y sub-box of the per-GPU grid (full
+    z, t and modes; REF_XY_DIV along x and y, so the run stays ~10-30 s of
+    host time).  Returns the cpu_baseline object (grid-pts·ch/s)."""
     import numpy as np
 
     import synth
     from oracle import spectral as sp
-    C = REF_WIDTH
-    vs = np.asarray(v[:, :C], dtype=np.float64)
-    dys = np.asarray(dy[:, :C], dtype=np.float64)
+    B, C, X, Y, Z, T = v.shape
+    xs, ys = max(2 * modes[0], X // REF_XY_DIV), max(2 * modes[1], Y // REF_XY_DIV)
+    vs = np.asarray(v[:, :, :xs, :ys], dtype=np.float64)
+    dys = np.asarray(dy[:, :, :xs, :ys], dtype=np.float64)
     s = synth.seed_for(CONFIG_INDEX, 0)
     R = synth.spectral_weights(C, C, modes, s + 1).astype(np.complex128)
     W, b = synth.channel_weights(C, s + 2)
@@ -474,9 +665,10 @@ def oracle_sample(args, v, dy, modes, repeats=1):
     units = vs.size          # grid points x channels of one layer, fwd+bwd
     cores = len(os.sched_getaffinity(0))
     return {"value": round(units / t, 1), "unit": "grid-pts·ch/s", "cores": cores, "kind": "oracle",
+            "threads": _blas_threads(),
             "sample": f"one DFNO block fwd+bwd (oracle.spectral.layer_fwd + layer_bwd, fp64 numpy, naive DFT "
-                      f"matrices) on the full per-GPU grid {list(v.shape[2:])}, width {C} of 20, batch 1; "
-                      f"{t:.2f} s wall",
+                      f"matrices) at full width {C} and modes {list(modes)} on the x/y sub-box "
+                      f"{[xs, ys, Z, T]} of the per-GPU grid {[X, Y, Z, T]}, batch {B}; {t:.2f} s wall",
             "seconds": round(t, 3)}
 
 
@@ -484,6 +676,10 @@ def oracle_sample(args, v, dy, modes, repeats=1):
 # reference arm: the oracle on the host cores (rank 0 only)
 # ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
+    """The reference arm of this tier: the fp64 oracle (as it stands) on the
+    box's host cores, each step one bounded sample of our arm's workload (one
+    DFNO block fwd+bwd at full width on an x/y sub-box, oracle_sample); rank 0
+    only, the other ranks exit without work."""
     if rank != 0:
         return
     import numpy as np
@@ -491,11 +687,14 @@ def run_reference(args, rank, world):
     import synth
     cfg = synth.CONFIGS[CONFIG_INDEX]
     lx, ly, Z, T = cfg["grid"]
-    modes = cfg["modes"]
-    shape = (1, REF_WIDTH, lx, ly, Z, T)
+    if cfg["name"] in STRONG and world in PGRIDS:     # our arm's per-GPU box at this N
+        lx, ly = lx // PGRIDS[world][0], ly // PGRIDS[world][1]
+    modes, C = cfg["modes"], cfg["width"]
+    xs, ys = max(2 * modes[0], lx // REF_XY_DIV), max(2 * modes[1], ly // REF_XY_DIV)
+    shape = (1, C, xs, ys, Z, T)
     s = synth.seed_for(CONFIG_INDEX, 0)
-    v = synth.field(shape, modes, s, cfg["shape"], n_waves=4)
-    dy = synth.cotangent(shape, s + 3)
+    v = synth.field(shape, modes, s, cfg["shape"], n_waves=4).astype(np.float32)
+    dy = synth.cotangent(shape, s + 3).astype(np.float32)
     for _ in range(args.warmup):
         oracle_sample(args, v, dy, modes)
     t0 = time.perf_counter()
@@ -508,11 +707,13 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "grid-pts·ch/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * wall / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded NS-shaped fields, random-init weights)",
-        "config": {"workload": f"{cfg['name']} per-GPU grid {lx}x{ly}x{Z}x{T}, modes {modes[0]}; oracle sample: one "
-                               f"DFNO block fwd+bwd at width {REF_WIDTH} of 20 per step (bounded CPU sample)",
-                   "grid": [lx, ly, Z, T], "width": REF_WIDTH, "modes": list(modes), "batch": 1},
+        "higher_is_better": True, "scaling": "strong" if cfg["name"] in STRONG else "weak", "vs_baseline": None,
+        "dtype": "f64",
+        "data": f"synthetic (seeded {'CO2' if cfg['shape'] == 'co2' else 'NS'}-shaped fields, random-init weights)",
+        "config": {"workload": WORKLOADS[cfg["name"]] + f"; oracle sample per step: one DFNO block fwd+bwd at width "
+                               f"{C} on the x/y sub-box {[xs, ys, Z, T]} of the per-GPU grid {[lx, ly, Z, T]}",
+                   "global_grid": list(cfg["grid"]), "sample_grid": [xs, ys, Z, T], "width": C,
+                   "modes": list(modes), "batch": 1},
         "cpu_baseline": cpu,
         "e2e": {"value": round(value, 1), "unit": "grid-pts·ch/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -531,8 +732,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly instead of as a CUDA graph")
     ap.add_argument("--network", action="store_true",
                     help="time the whole network's training step (lift, blocks, projection, loss, backward, Adam)")
-    ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c2",
-                    help="BASELINE.json workload (default c2 = configs[1]; c3 strong, c4 weak, c5 strong)")
+    ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c3",
+                    help="BASELINE.json workload (default c3 = configs[2], strong; c2 configs[1]; c4 weak; c5 strong)")
+    ap.add_argument("--no-phases", action="store_true", help="skip the per-phase (fwd inference / fwd train / bwd) timing")
     args = ap.parse_args()
     global CONFIG_INDEX
     CONFIG_INDEX = int(args.config[1])
@@ -547,6 +749,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if os.environ.get("FNO_ABLATE") or os.environ.get("FNO_LIB"):
+        raise SystemExit("bench.py: FNO_ABLATE / FNO_LIB select profiling-only builds; unset them for a bench line")
     if world not in PGRIDS:
         raise SystemExit(f"unsupported world size {world} (1, 2, 4, 8)")
     if world > 1:

@@ -117,11 +117,24 @@ fno_status fno_plan_set_workspace(fno_plan_t plan, void* dptr, size_t bytes);
  * owners' receive buffers -- and each exchange reduces to a barrier (a one-int
  * NCCL all-reduce).  Only the retained-mode slab crosses NVLink, as before.
  * Stream-ordered on `stream` (synchronised once inside).  No-op when P == 1.
- * The workspace must stay allocated for the plan's lifetime; the mappings are
- * closed by fno_plan_destroy.  FNO_ERR_PLAN if the GPUs cannot access each
- * other's memory, FNO_ERR_CUDA / FNO_ERR_NCCL on a failed mapping or
- * all-gather (the plan then keeps using NCCL send/recv exchanges). */
+ * The workspace must stay allocated for the plan's lifetime, and
+ * fno_plan_set_workspace / fno_plan_set_io_partition are rejected
+ * (FNO_ERR_INVALID_STATE) once the peers are connected; the mappings are closed
+ * by fno_plan_destroy.  The choice is collective: if any rank cannot export its
+ * workspace or open a peer's (CUDA IPC refused, no peer access, ...), every rank
+ * returns FNO_OK and keeps the NCCL send/recv exchanges (query with
+ * fno_plan_peer_enabled).  FNO_ERR_CUDA / FNO_ERR_NCCL only when the handle
+ * all-gather itself fails. */
 fno_status fno_plan_connect_peers(fno_plan_t plan, void* stream);
+/* Which pass C kernel the plan launches for mode 0 (spectral u), 1 (layer
+ * forward), 2 (layer backward): info = {family, padded width, input-ring
+ * stages / tile buffers, dynamic shared memory bytes}; family 4 = the
+ * warp-specialised tcgen05 kernel (pass_c4), 3 = pass_c3, 2 = pass_c2 (FFMA),
+ * 1 = the generic pass_c.  The family-4 launch falls back to the next family
+ * when the tensors' alignment rules out its TMA view. */
+fno_status fno_plan_pass_c_info(fno_plan_t plan, int mode, int64_t info[4]);
+/* *enabled = 1 if fno_plan_connect_peers switched the exchanges to peer stores. */
+fno_status fno_plan_peer_enabled(fno_plan_t plan, int* enabled);
 /* Caller-side partition of the fields (the paper's App. A 3-D
  * spatial and temporal partitions): io_pgrid = (px', py', pz', pt')
  * over the same P ranks (row-major, each extent divisible by its part).  The
@@ -245,6 +258,37 @@ fno_status fno_adam(float* p, const float* g, float* m, float* v, size_t n, floa
 fno_status fno_repartition(fno_comm_t comm, int ndim, const int64_t* global_shape, const int32_t* src_pgrid,
                            const int32_t* dst_pgrid, size_t elem_bytes, const void* src_local, void* dst_local,
                            void* workspace, size_t* ws_bytes, void* stream);
+
+/* ---- plan groups: a P-rank decomposition in ONE process on ONE device ------ */
+/* The decomposed data path of Eq. sconv_dist without P GPUs: plan
+ * r (r = 0..n-1) is rank r of the same n-rank problem, created on a
+ * fno_comm_init_local(n, r) communicator, its workspace set on the common
+ * device.  fno_group_connect points every plan's exchange destinations at the
+ * other plans' workspaces (the peer-store exchange of fno_plan_connect_peers
+ * with same-device pointers), after which the plans are usable only through
+ * the fno_group_* calls.  Each group call runs one stage for every rank before
+ * the next stage (pass A of all ranks, then pass B, then pass C, then the
+ * rank-ordered dW / db sum), all on `stream`, so stream order is the exchange
+ * barrier and no rank ever waits for another.  Arrays hold one pointer per
+ * rank (the rank's local box / kz block, as in the per-plan calls; vhat_save
+ * entries and the vhat_save / z_save / dv / dR arrays themselves nullable as
+ * in the per-plan calls); W, b, dW, db are single (replicated) tensors and dW
+ * / db come back summed over the ranks in rank order.  Errors as in the
+ * per-plan calls; FNO_ERR_INVALID_STATE for plans that are not a connected
+ * group in rank order. */
+fno_status fno_group_connect(int n, fno_plan_t* plans);
+fno_status fno_group_spectral_conv_fwd(int n, fno_plan_t* plans, const float* const* v, const void* const* R,
+                                       float* const* u, void* const* vhat_save, void* stream);
+fno_status fno_group_spectral_conv_bwd(int n, fno_plan_t* plans, const float* const* g, const void* const* R,
+                                       const void* const* vhat_saved, float* const* dv, void* const* dR,
+                                       int accumulate, void* stream);
+fno_status fno_group_layer_fwd(int n, fno_plan_t* plans, const float* const* v, const void* const* R, const float* W,
+                               const float* b, float* const* y, float* const* z_save, void* const* vhat_save,
+                               void* stream);
+fno_status fno_group_layer_bwd(int n, fno_plan_t* plans, const float* const* v, const float* const* z_saved,
+                               const void* const* vhat_saved, const float* const* dy, const void* const* R,
+                               const float* W, float* const* dv, void* const* dR, float* dW, float* db,
+                               int accumulate, void* stream);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* When enabled, every stage of every call on this plan (pass A, exchange 1,

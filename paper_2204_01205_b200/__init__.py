@@ -81,6 +81,8 @@ def lib() -> ctypes.CDLL:
             "fno_plan_workspace_size": [vp, P(sz)],
             "fno_plan_set_workspace": [vp, vp, sz],
             "fno_plan_connect_peers": [vp, vp],
+            "fno_plan_peer_enabled": [vp, P(i32)],
+            "fno_plan_pass_c_info": [vp, i32, P(ctypes.c_int64)],
             "fno_plan_local_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
             "fno_plan_set_io_partition": [vp, P(ctypes.c_int32)],
             "fno_plan_io_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
@@ -97,6 +99,11 @@ def lib() -> ctypes.CDLL:
             "fno_net_loss": [vp, vp, vp, vp, vp, vp],
             "fno_net_bwd": [vp, P(_NetDesc), P(_NetParams), vp, P(_NetActs), vp, vp, P(_NetParams), vp, vp, vp, vp],
             "fno_comm_allreduce": [vp, vp, sz, i32, vp],
+            "fno_group_connect": [i32, vp],
+            "fno_group_spectral_conv_fwd": [i32, vp, vp, vp, vp, vp, vp],
+            "fno_group_spectral_conv_bwd": [i32, vp, vp, vp, vp, vp, vp, i32, vp],
+            "fno_group_layer_fwd": [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "fno_group_layer_bwd": [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
             "fno_adam": [vp, vp, vp, vp, sz, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, vp],
         }
         for name, args in sig.items():
@@ -254,6 +261,12 @@ class Plan:
         _check(lib().fno_plan_connect_peers(self.handle, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
                "fno_plan_connect_peers")
 
+    def peer_enabled(self) -> bool:
+        """True if the exchanges are direct NVLink peer stores (collective decision)."""
+        e = ctypes.c_int32()
+        _check(lib().fno_plan_peer_enabled(self.handle, ctypes.byref(e)), "fno_plan_peer_enabled")
+        return bool(e.value)
+
     def workspace_size(self) -> int:
         n = ctypes.c_size_t()
         _check(lib().fno_plan_workspace_size(self.handle, ctypes.byref(n)), "fno_plan_workspace_size")
@@ -321,6 +334,18 @@ class Plan:
             self.destroy()
         except Exception:
             pass
+
+
+def plan_pass_c_kernels(plan: Plan) -> dict:
+    """{mode: {family, width, stages, smem}} of the pass C kernels the plan selected."""
+    fam = {4: "pass_c4 (warp-specialised, TMA ring, tcgen05)", 3: "pass_c3 (tcgen05 1x1)", 2: "pass_c2 (FFMA)",
+           1: "pass_c (generic)"}
+    out = {}
+    for m, name in enumerate(("u", "fwd", "bwd")):
+        info = (ctypes.c_int64 * 4)()
+        _check(lib().fno_plan_pass_c_info(plan.handle, m, info), "fno_plan_pass_c_info")
+        out[name] = {"family": fam.get(info[0], info[0]), "width": info[1], "stages": info[2], "smem": info[3]}
+    return out
 
 
 def kernel_launches() -> int:
@@ -436,6 +461,56 @@ def adam(p, g, m, v, step: int, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, strea
            "fno_adam")
 
 
+# ---- plan groups: a P-rank decomposition in one process on one device ---------
+
+def _parr(ts):
+    """ctypes array of device pointers (None -> NULL entry); None -> NULL array."""
+    if ts is None:
+        return None
+    return (ctypes.c_void_p * len(ts))(*[_ptr(t) for t in ts])
+
+
+class PlanGroup:
+    """The P ranks of an x/y decomposition (pgrid (px, py)) as P plans on one
+    device (fno_group_connect).  ``plans[r]`` gives rank r's local box, owned kz
+    block and shapes; the compute calls take one tensor per rank."""
+
+    def __init__(self, problem: Problem, device=None):
+        n = int(problem.pgrid[0]) * int(problem.pgrid[1])
+        self.problem, self.n = problem, n
+        self.comms = [Comm.local(n, r) for r in range(n)]
+        self.plans = [Plan(problem, self.comms[r], device=device, peer_exchange=False) for r in range(n)]
+        self._h = (ctypes.c_void_p * n)(*[p.handle.value for p in self.plans])
+        _check(lib().fno_group_connect(n, self._h), "fno_group_connect")
+
+    def destroy(self):
+        for p in self.plans:
+            p.destroy()
+        for c in self.comms:
+            c.destroy()
+
+
+def group_spectral_conv_fwd(g: PlanGroup, vs, Rs, us, vhs=None, stream=None):
+    _check(lib().fno_group_spectral_conv_fwd(g.n, g._h, _parr(vs), _parr(Rs), _parr(us), _parr(vhs), _stream(stream)),
+           "fno_group_spectral_conv_fwd")
+
+
+def group_spectral_conv_bwd(g: PlanGroup, gs, Rs, vhs=None, dvs=None, dRs=None, accumulate=False, stream=None):
+    _check(lib().fno_group_spectral_conv_bwd(g.n, g._h, _parr(gs), _parr(Rs), _parr(vhs), _parr(dvs), _parr(dRs),
+                                             int(bool(accumulate)), _stream(stream)), "fno_group_spectral_conv_bwd")
+
+
+def group_layer_fwd(g: PlanGroup, vs, Rs, W, b, ys, zs=None, vhs=None, stream=None):
+    _check(lib().fno_group_layer_fwd(g.n, g._h, _parr(vs), _parr(Rs), _ptr(W), _ptr(b), _parr(ys), _parr(zs),
+                                     _parr(vhs), _stream(stream)), "fno_group_layer_fwd")
+
+
+def group_layer_bwd(g: PlanGroup, vs, zs, vhs, dys, Rs, W, dvs, dRs, dW, db=None, accumulate=False, stream=None):
+    _check(lib().fno_group_layer_bwd(g.n, g._h, _parr(vs), _parr(zs), _parr(vhs), _parr(dys), _parr(Rs), _ptr(W),
+                                     _parr(dvs), _parr(dRs), _ptr(dW), _ptr(db), int(bool(accumulate)),
+                                     _stream(stream)), "fno_group_layer_bwd")
+
+
 def repartition(comm: Optional[Comm], global_shape, src_pgrid, dst_pgrid, src_local, dst_local, stream=None):
     """R_{P->Q}; the adjoint is the call with the pgrids swapped."""
     import torch
@@ -456,5 +531,6 @@ def repartition(comm: Optional[Comm], global_shape, src_pgrid, dst_pgrid, src_lo
     return ws  # keep alive until the stream has consumed it
 
 
-__all__ = ["Problem", "Comm", "Plan", "FnoError", "lib", "spectral_conv_fwd", "spectral_conv_bwd", "layer_fwd",
-           "layer_bwd", "repartition", "kernel_launches", "LIB_PATH"]
+__all__ = ["Problem", "Comm", "Plan", "PlanGroup", "FnoError", "lib", "spectral_conv_fwd", "spectral_conv_bwd",
+           "layer_fwd", "layer_bwd", "group_spectral_conv_fwd", "group_spectral_conv_bwd", "group_layer_fwd",
+           "group_layer_bwd", "repartition", "kernel_launches", "LIB_PATH"]

@@ -63,6 +63,8 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+static const bool kC4Layer = false;   // pass_c4 for the layer forward / backward
+
 enum Stage { ST_PASS_A, ST_EX1, ST_B_YF, ST_B_XF, ST_MIX, ST_B_XI, ST_B_YI, ST_EX2, ST_PASS_C, ST_DW, ST_N };
 static const char* kStageNames[2 * ST_N] = {
     "fwd.pass_a", "fwd.exchange_1", "fwd.b_y_fwd", "fwd.b_x_fwd", "fwd.mix", "fwd.b_x_inv", "fwd.b_y_inv", "fwd.exchange_2", "fwd.pass_c", "fwd.unused",
@@ -94,13 +96,17 @@ struct fno_plan_s {
   int LZ, LT, LX, LY;
   int Qz, Qt, Qx, Qy;
   int num_sms = 148;
-  int grid_c = 1, grid_c_bwd = 1;
+  int grid_c = 1, grid_c_bwd = 1, grid_c_u = 1;
   size_t smem_a[3] = {0, 0, 0}, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
   int np_a[3] = {1, 1, 1}, ns_a[3] = {2, 2, 2}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
   int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
   int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
   int c2nx[3] = {2, 2, 2};                     // pass_c2 X tile buffers
   int c3cp[3] = {0, 0, 0};                     // > 0: tensor-core pass_c3 kernel with that padded width
+  int c4cp[3] = {0, 0, 0};                     // > 0: warp-specialised pass_c4 kernel (preferred)
+  int c4ns[3] = {0, 0, 0};                     // its input-ring depth
+  size_t c4smem[3] = {0, 0, 0};
+  int c4grid = 1;                              // one CTA per SM
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -108,6 +114,7 @@ struct fno_plan_s {
   size_t o_slab_xy, o_slab_kz, o_h, o_vhat, o_what, o_ghat, o_dwpart, o_dwall, o_dwloc, o_dz, o_bar, o_ipc, total;
   // peer exchange (fno_plan_connect_peers): every rank's workspace mapped over NVLink
   int peer = 0;
+  int group = 0;                  // fno_group_connect: one of P plans of one process / device
   std::vector<char*> peer_ws;     // [P] workspace base of rank d in this process's address space
   std::vector<void*> ipc_opened;  // mappings to close at destroy
   size_t n_slab_xy, n_slab_kz, n_h, n_mode;
@@ -270,6 +277,7 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   p->iy = rank % p->py;
   p->X = pb->grid[0]; p->Y = pb->grid[1]; p->Z = pb->grid[2]; p->T = pb->grid[3];
   p->Xl = p->X / p->px; p->Yl = p->Y / p->py;
+  p->io[0] = p->px; p->io[1] = p->py; p->io[2] = 1; p->io[3] = 1;   // the caller's partition is the plan's until set
   p->B = pb->batch; p->C = pb->width;
   p->mx = pb->modes[0]; p->my = pb->modes[1]; p->mz = pb->modes[2]; p->mt = pb->modes[3];
   p->act_gelu = (pb->flags & FNO_ACT_NONE) ? 0 : 1;
@@ -322,7 +330,11 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
   pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
   {
+#ifdef FNO_DEV_KNOBS   // development builds only: FNO_PASS_C_LEGACY=1 keeps the generic pass_c kernels
     const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
+#else
+    const char* legacy = nullptr;
+#endif
     if (!(legacy && legacy[0] == '1')) {
       int cp, tch, vw, nx;
       size_t sm;
@@ -334,6 +346,20 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
       }
       if (pass_c3_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &sm)) {
         p->c3cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->smem_c_fwd = sm;
+      }
+#ifdef FNO_DEV_KNOBS
+      const char* c4e = std::getenv("FNO_PASS_C4");
+      const bool c4_on = !(c4e && c4e[0] == '0');
+#else
+      const bool c4_on = true;
+#endif
+      for (int m = 0; m < 3 && c4_on; ++m) {
+        // layer epilogues: pass_c4 only where no pass_c2 / pass_c3 kernel covers the shape (being tuned)
+        if (m != EPI_U && (p->c2cp[m] > 0 || p->c3cp[m] > 0) && !kC4Layer) continue;
+        int ns;
+        if (pass_c4_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, m, &cp, &ns, &sm)) {
+          p->c4cp[m] = cp; p->c4ns[m] = ns; p->c4smem[m] = sm;
+        }
       }
     }
   }
@@ -358,7 +384,9 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   };
   p->grid_c = grid_for(p->smem_c_fwd);
   p->grid_c_bwd = grid_for(p->smem_c_bwd);
-  p->max_grid_c = p->grid_c_bwd;
+  p->grid_c_u = grid_for(p->smem_c_u);
+  p->c4grid = int(std::max<long long>(1, std::min<long long>(n_cols, p->num_sms)));
+  p->max_grid_c = std::max(p->grid_c_bwd, p->c4grid);
 
   // workspace layout
   p->mloc = 4LL * p->mx * p->my * p->nkz * p->mt;
@@ -401,6 +429,8 @@ extern "C" fno_status fno_plan_set_workspace(fno_plan_t p, void* dptr, size_t by
   if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_workspace: NULL plan");
   if (!dptr || bytes < p->total) return fail(FNO_ERR_WORKSPACE, "fno_plan_set_workspace: workspace NULL or smaller than fno_plan_workspace_size");
   if (reinterpret_cast<uintptr_t>(dptr) & 255) return fail(FNO_ERR_WORKSPACE, "fno_plan_set_workspace: workspace must be 256-byte aligned");
+  // the peers hold mappings of the current workspace (fno_plan_connect_peers)
+  if (p->peer) return fail(FNO_ERR_INVALID_STATE, "fno_plan_set_workspace: peers are connected to the current workspace");
   p->ws = dptr;
   p->ws_bytes = bytes;
   return FNO_OK;
@@ -420,25 +450,35 @@ extern "C" fno_status fno_plan_connect_peers(fno_plan_t p, void* stream) {
   if (!range) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return fail(FNO_ERR_CUDA, "fno_plan_connect_peers: cuMemGetAddressRange unavailable");
-    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    else
+      cudaGetLastError();
   }
-  CUdeviceptr base = 0;
-  size_t alloc = 0;
-  if (range(&base, &alloc, reinterpret_cast<CUdeviceptr>(p->ws)) != CUDA_SUCCESS)
-    return fail(FNO_ERR_CUDA, "fno_plan_connect_peers: workspace allocation range");
+  // Every rank contributes a record even when it cannot export its workspace
+  // (no driver entry point, an allocator whose memory CUDA IPC refuses, ...),
+  // so the all-gather below never leaves a rank behind; whether peer stores
+  // are used is then decided collectively (all ranks or none).  Peer access is
+  // not pre-checked with device ordinals (those are process-local, e.g. every
+  // rank sees device 0 under per-rank CUDA_VISIBLE_DEVICES):
+  // cudaIpcOpenMemHandle itself decides.
   struct Rec {
     cudaIpcMemHandle_t h;
     unsigned long long off;
-    int dev;
+    int ok;
   };
   static_assert(sizeof(Rec) <= 256, "handle record");
   Rec mine{};
-  FNO_CUDA(cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)), "fno_plan_connect_peers: cudaIpcGetMemHandle");
-  mine.off = reinterpret_cast<CUdeviceptr>(p->ws) - base;
-  FNO_CUDA(cudaGetDevice(&mine.dev), "fno_plan_connect_peers: cudaGetDevice");
+  CUdeviceptr base = 0;
+  size_t alloc = 0;
+  if (range && range(&base, &alloc, reinterpret_cast<CUdeviceptr>(p->ws)) == CUDA_SUCCESS &&
+      cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) == cudaSuccess) {
+    mine.off = reinterpret_cast<CUdeviceptr>(p->ws) - base;
+    mine.ok = 1;
+  } else {
+    cudaGetLastError();
+  }
   unsigned char* dbuf = static_cast<unsigned char*>(p->ws) + p->o_ipc;
   FNO_CUDA(cudaMemcpyAsync(dbuf + size_t(p->rank) * 256, &mine, sizeof mine, cudaMemcpyHostToDevice, st), "ipc h2d");
   FNO_NCCL(ncclAllGather(dbuf + size_t(p->rank) * 256, dbuf, 256, ncclUint8, p->comm->nccl, st), "ipc all-gather");
@@ -446,23 +486,55 @@ extern "C" fno_status fno_plan_connect_peers(fno_plan_t p, void* stream) {
   FNO_CUDA(cudaMemcpyAsync(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost, st), "ipc d2h");
   FNO_CUDA(cudaStreamSynchronize(st), "fno_plan_connect_peers: sync");
   std::vector<char*> bases(p->P, nullptr);
-  for (int d = 0; d < p->P; ++d) {
+  std::vector<void*> opened;
+  int ok = 1;
+  for (int d = 0; d < p->P && ok; ++d) {
     Rec r;
     std::memcpy(&r, all.data() + size_t(d) * 256, sizeof r);
+    if (!r.ok) { ok = 0; break; }
     if (d == p->rank) {
       bases[d] = static_cast<char*>(p->ws);
       continue;
     }
-    int can = 0;
-    FNO_CUDA(cudaDeviceCanAccessPeer(&can, mine.dev, r.dev), "cudaDeviceCanAccessPeer");
-    if (!can) return fail(FNO_ERR_PLAN, "fno_plan_connect_peers: no peer access between the ranks' GPUs");
     void* m = nullptr;
-    FNO_CUDA(cudaIpcOpenMemHandle(&m, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-    p->ipc_opened.push_back(m);
+    if (cudaIpcOpenMemHandle(&m, r.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    opened.push_back(m);
     bases[d] = static_cast<char*>(m) + r.off;
   }
+  // collective decision: peer stores only if every rank mapped every peer
+  int* flag = reinterpret_cast<int*>(dbuf + size_t(p->rank) * 256);
+  FNO_CUDA(cudaMemcpyAsync(flag, &ok, sizeof ok, cudaMemcpyHostToDevice, st), "peer flag h2d");
+  FNO_NCCL(ncclAllReduce(flag, flag, 1, ncclInt, ncclMin, p->comm->nccl, st), "peer flag all-reduce");
+  int all_ok = 0;
+  FNO_CUDA(cudaMemcpyAsync(&all_ok, flag, sizeof all_ok, cudaMemcpyDeviceToHost, st), "peer flag d2h");
+  FNO_CUDA(cudaStreamSynchronize(st), "fno_plan_connect_peers: sync");
+  if (!all_ok) {   // every rank keeps the NCCL send/recv exchanges
+    for (void* m : opened) cudaIpcCloseMemHandle(m);
+    return FNO_OK;
+  }
+  p->ipc_opened.insert(p->ipc_opened.end(), opened.begin(), opened.end());
   p->peer_ws = bases;
   p->peer = 1;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_peer_enabled(fno_plan_t p, int* enabled) {
+  if (!p || !enabled) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_peer_enabled: NULL argument");
+  *enabled = p->peer;
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_pass_c_info(fno_plan_t p, int mode, int64_t info[4]) {
+  if (!p || !info || mode < 0 || mode > 2) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_pass_c_info: bad arguments");
+  const int m = mode == 0 ? EPI_U : (mode == 1 ? EPI_FWD : EPI_BWD);
+  if (p->c4cp[m] > 0) { info[0] = 4; info[1] = p->c4cp[m]; info[2] = p->c4ns[m]; info[3] = int64_t(p->c4smem[m]); }
+  else if (p->c3cp[m] > 0) { info[0] = 3; info[1] = p->c3cp[m]; info[2] = 0; info[3] = int64_t(p->smem_c_fwd); }
+  else if (p->c2cp[m] > 0) { info[0] = 2; info[1] = p->c2cp[m]; info[2] = p->c2nx[m]; info[3] = int64_t(m == EPI_FWD ? p->smem_c_fwd : p->smem_c_bwd); }
+  else { info[0] = 1; info[1] = p->C; info[2] = 0; info[3] = int64_t(m == EPI_U ? p->smem_c_u : (m == EPI_FWD ? p->smem_c_fwd : p->smem_c_bwd)); }
   return FNO_OK;
 }
 
@@ -566,7 +638,7 @@ fno_status peer_barrier(fno_plan_t p, int stage, const char* what, cudaStream_t 
 }
 
 fno_status exchange_fwd(fno_plan_t p, cudaStream_t st) {
-  if (p->P == 1) return FNO_OK;
+  if (p->P == 1 || p->group) return FNO_OK;   // group: stream order is the barrier
   if (p->peer) return peer_barrier(p, ST_EX1, "exchange 1 (peer barrier)", st);
   const KzSlab s = make_kzslab(p);
   const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;  // complex per kz plane
@@ -586,7 +658,7 @@ fno_status exchange_fwd(fno_plan_t p, cudaStream_t st) {
 
 // exchange 2 (adjoint): x/y-destination ordered -> kz-owner ordered
 fno_status exchange_bwd(fno_plan_t p, cudaStream_t st) {
-  if (p->P == 1) return FNO_OK;
+  if (p->P == 1 || p->group) return FNO_OK;
   if (p->peer) return peer_barrier(p, ST_EX2, "exchange 2 (peer barrier)", st);
   const KzSlab s = make_kzslab(p);
   const size_t per = size_t(p->B) * p->Xl * p->Yl * p->C * p->mt;
@@ -659,10 +731,12 @@ PassCParams make_c(fno_plan_t p, int mode) {
   c.TCH = p->tch[mode];
   c.VW = p->vw[mode];
   c.NX = p->c2nx[mode];
+#ifdef FNO_ABLATE_BUILD
   {
     static const int ablate = [] { const char* e = std::getenv("FNO_ABLATE"); return e ? std::atoi(e) : 0; }();
     c.ablate = ablate;
   }
+#endif
   c.in = wsp<float2>(p, p->o_slab_xy);
   c.n_cols = (long long)p->B * p->Xl * p->Yl;
   c.B = p->B; c.C = p->C; c.Xl = int(p->Xl); c.Yl = int(p->Yl); c.Z = int(p->Z); c.T = int(p->T);
@@ -673,7 +747,22 @@ PassCParams make_c(fno_plan_t p, int mode) {
   return c;
 }
 
-cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c, int mode, int grid, size_t smem, cudaStream_t st) {
+// the preferred pass C kernel for the mode; *grid_used: its CTA count (the
+// number of dW / db partial rows of the backward)
+cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c0, int mode, int grid, size_t smem, cudaStream_t st,
+                       int* grid_used = nullptr) {
+  if (p->c4cp[mode] > 0) {
+    PassCParams c = c0;
+    c.NX = p->c4ns[mode];
+    cudaError_t e = launch_pass_c4(c, p->LZ, p->LT, p->c4cp[mode], mode, p->c4grid, p->c4smem[mode], st);
+    if (e != cudaErrorNotSupported) {
+      if (grid_used) *grid_used = p->c4grid;
+      return e;
+    }
+    cudaGetLastError();   // alignment rules out the TMA view: older kernels below
+  }
+  if (grid_used) *grid_used = grid;
+  const PassCParams& c = c0;
   if (p->c3cp[mode] > 0) return launch_pass_c3(c, p->LZ, p->LT, p->c3cp[mode], grid, smem, st);
   if (p->c2cp[mode] > 0) return launch_pass_c2(c, p->LZ, p->LT, p->c2cp[mode], mode, grid, smem, st);
   return launch_pass_c(c, p->LZ, p->LT, mode, grid, smem, st);
@@ -682,7 +771,8 @@ cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c, int mode, int grid, s
 fno_status check_ready(fno_plan_t p, const char* who) {
   if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": NULL plan");
   if (!p->ws) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": workspace not set (fno_plan_set_workspace)");
-  if (p->P > 1 && (!p->comm || !p->comm->nccl)) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": communicator missing");
+  if (p->P > 1 && !p->group && (!p->comm || !p->comm->nccl))
+    return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": communicator missing");
   return FNO_OK;
 }
 
@@ -692,27 +782,35 @@ fno_status check_ready(fno_plan_t p, const char* who) {
     if (_s != FNO_OK) return _s;  \
   } while (0)
 
-// forward spectral chain up to the second exchange; the slab for pass C is
-// left in the x/y-ordered buffer.  vhat: where V^ goes (scratch or saved).
-fno_status spectral_fwd_to_slab(fno_plan_t p, const float* v, const float2* R, float2* vhat, cudaStream_t st) {
-  FNO_TRY(run_pass_a(p, v, nullptr, MODE_V, st));
-  FNO_TRY(exchange_fwd(p, st));
+// ---- the layer as stages ----------------------------------------------------
+// A stage is a sequence of this rank's launches that never waits for another
+// rank; the exchanges sit between stages.  One process per GPU runs the stages
+// of one plan back to back with the exchanges in between; a plan group
+// (fno_group_*, one device) runs each stage for every rank before the next.
+
+// forward, stage A: pass A (t, z transforms of v, I_1) -> the kz owners' slabs
+fno_status sf_stage_a(fno_plan_t p, const float* v, cudaStream_t st) { return run_pass_a(p, v, nullptr, MODE_V, st); }
+
+// forward, stage B: pass B on the owned kz block (y, x forward -> V^; mixing
+// with R on the owned modes; x, y inverse -> the x/y owners' slabs)
+fno_status sf_stage_b(fno_plan_t p, const float2* R, float2* vhat, cudaStream_t st) {
   FNO_TRY(run_b_fwd(p, vhat, st));
   if (p->nkz > 0) {
     MixParams m = make_mix(p);
     m.vhat = vhat; m.R = R; m.what = wsp<float2>(p, p->o_what);
     FNO_LAUNCH(p, ST_MIX, launch_mix_fwd(m, st), "mixing (forward)");
   }
-  FNO_TRY(run_b_inv(p, wsp<float2>(p, p->o_what), st));
-  FNO_TRY(exchange_bwd(p, st));
-  return FNO_OK;
+  return run_b_inv(p, wsp<float2>(p, p->o_what), st);
 }
 
-// adjoint spectral chain on g (input already in the pass-A form selected by mode)
-fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1, int mode, const float2* R,
-                                const float2* vhat_saved, float2* dR, int accumulate, cudaStream_t st) {
-  FNO_TRY(run_pass_a(p, in0, in1, mode, st));
-  FNO_TRY(exchange_fwd(p, st));
+// adjoint, stage A: pass A on g (or dz = dy sigma'(z) when mode says so)
+fno_status sb_stage_a(fno_plan_t p, const float* in0, const float* in1, int mode, cudaStream_t st) {
+  return run_pass_a(p, in0, in1, mode, st);
+}
+
+// adjoint, stage B: pass B with R^H, and dR on the owned modes (no comm)
+fno_status sb_stage_b(fno_plan_t p, const float2* R, const float2* vhat_saved, float2* dR, int accumulate,
+                      cudaStream_t st) {
   float2* ghat = wsp<float2>(p, p->o_ghat);
   FNO_TRY(run_b_fwd(p, ghat, st));
   if (p->nkz > 0) {
@@ -721,62 +819,113 @@ fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1
     m.dR = dR; m.accumulate = accumulate;
     FNO_LAUNCH(p, ST_MIX, launch_mix_bwd(m, st), "mixing (backward)");
   }
-  FNO_TRY(run_b_inv(p, wsp<float2>(p, p->o_what), st));
-  FNO_TRY(exchange_bwd(p, st));
-  return FNO_OK;
+  return run_b_inv(p, wsp<float2>(p, p->o_what), st);
 }
 
-}  // namespace
-
-static fno_status xy_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
-                                            void* stream) {
-  FNO_TRY(check_ready(p, "fno_spectral_conv_fwd"));
-  p->dir = 0;
-  if (!v || !u || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_fwd: NULL data pointer");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
-  FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
+// stage C: pass C (inverse z, t) with the plain output u = S v (or S^T g)
+fno_status stage_c_u(fno_plan_t p, float* out, cudaStream_t st) {
   PassCParams c = make_c(p, EPI_U);
-  c.out = u;
-  FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (u)");
+  c.out = out;
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_U, p->grid_c_u, p->smem_c_u, st), "pass C (u)");
   return FNO_OK;
 }
 
-static fno_status xy_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
-                                            float* dv, void* dR, int accumulate, void* stream) {
-  FNO_TRY(check_ready(p, "fno_spectral_conv_bwd"));
-  p->dir = 1;
-  if (!g || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: NULL g or R");
-  if (dR && !vhat_saved && p->nkz > 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: dR requires vhat_saved");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  FNO_TRY(spectral_bwd_to_slab(p, g, nullptr, MODE_V, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
-                               static_cast<float2*>(dR), accumulate, st));
-  if (dv) {
-    PassCParams c = make_c(p, EPI_U);
-    c.out = dv;
-    FNO_LAUNCH(p, ST_PASS_C, launch_pass_c(c, p->LZ, p->LT, EPI_U, p->grid_c, p->smem_c_u, st), "pass C (adjoint u)");
-  }
-  return FNO_OK;
-}
-
-static fno_status xy_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
-                                    float* z_save, void* vhat_save, void* stream) {
-  FNO_TRY(check_ready(p, "fno_layer_fwd"));
-  p->dir = 0;
-  if (!v || !W || !y || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_fwd: NULL data pointer");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
-  FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
+// stage C of the layer forward: z = W v + b + u, y = sigma(z)
+fno_status stage_c_fwd(fno_plan_t p, const float* v, const float* W, const float* b, float* y, float* z_save,
+                       cudaStream_t st) {
   PassCParams c = make_c(p, EPI_FWD);
   c.v = v; c.W = W; c.bias = b; c.out = y; c.zsave = z_save;
   FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
   return FNO_OK;
 }
 
+// stage C of the layer backward: dv = W^T dz + S^T dz and the per-CTA dW / db
+// partials; then this rank's fixed-order partial sum (into `loc`, or straight
+// into dW / db when loc is NULL)
+fno_status stage_c_bwd(fno_plan_t p, const float* v, const float* dz, const float* W, float* dv, float* loc, float* dW,
+                       float* db, int accumulate, cudaStream_t st) {
+  PassCParams c = make_c(p, EPI_BWD);
+  c.v = v; c.dy = dz; c.W = W; c.out = dv;
+  c.dWpart = wsp<float>(p, p->o_dwpart);
+  int nparts = p->grid_c_bwd;
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st, &nparts), "pass C (layer backward)");
+  const int len = p->C * p->C + p->C;
+  if (!loc) {
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, nparts, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
+  } else {
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, nparts, len, len, loc, nullptr, 0, st), "dW/db local reduction");
+  }
+  return FNO_OK;
+}
+
+// forward spectral chain up to the second exchange; the slab for pass C is
+// left in the x/y-ordered buffer.  vhat: where V^ goes (scratch or saved).
+fno_status spectral_fwd_to_slab(fno_plan_t p, const float* v, const float2* R, float2* vhat, cudaStream_t st) {
+  FNO_TRY(sf_stage_a(p, v, st));
+  FNO_TRY(exchange_fwd(p, st));
+  FNO_TRY(sf_stage_b(p, R, vhat, st));
+  return exchange_bwd(p, st);
+}
+
+// adjoint spectral chain on g (input already in the pass-A form selected by mode)
+fno_status spectral_bwd_to_slab(fno_plan_t p, const float* in0, const float* in1, int mode, const float2* R,
+                                const float2* vhat_saved, float2* dR, int accumulate, cudaStream_t st) {
+  FNO_TRY(sb_stage_a(p, in0, in1, mode, st));
+  FNO_TRY(exchange_fwd(p, st));
+  FNO_TRY(sb_stage_b(p, R, vhat_saved, dR, accumulate, st));
+  return exchange_bwd(p, st);
+}
+
+fno_status not_grouped(fno_plan_t p, const char* who) {
+  if (p && p->group) return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": the plan belongs to a plan group (use fno_group_*)");
+  return FNO_OK;
+}
+
+}  // namespace
+
+static fno_status xy_spectral_conv_fwd(fno_plan_t p, const float* v, const void* R, float* u, void* vhat_save,
+                                       void* stream) {
+  FNO_TRY(check_ready(p, "fno_spectral_conv_fwd"));
+  FNO_TRY(not_grouped(p, "fno_spectral_conv_fwd"));
+  p->dir = 0;
+  if (!v || !u || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_fwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
+  FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
+  return stage_c_u(p, u, st);
+}
+
+static fno_status xy_spectral_conv_bwd(fno_plan_t p, const float* g, const void* R, const void* vhat_saved,
+                                       float* dv, void* dR, int accumulate, void* stream) {
+  FNO_TRY(check_ready(p, "fno_spectral_conv_bwd"));
+  FNO_TRY(not_grouped(p, "fno_spectral_conv_bwd"));
+  p->dir = 1;
+  if (!g || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: NULL g or R");
+  if (dR && !vhat_saved && p->nkz > 0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_spectral_conv_bwd: dR requires vhat_saved");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FNO_TRY(spectral_bwd_to_slab(p, g, nullptr, MODE_V, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
+                               static_cast<float2*>(dR), accumulate, st));
+  if (dv) FNO_TRY(stage_c_u(p, dv, st));
+  return FNO_OK;
+}
+
+static fno_status xy_layer_fwd(fno_plan_t p, const float* v, const void* R, const float* W, const float* b, float* y,
+                               float* z_save, void* vhat_save, void* stream) {
+  FNO_TRY(check_ready(p, "fno_layer_fwd"));
+  FNO_TRY(not_grouped(p, "fno_layer_fwd"));
+  p->dir = 0;
+  if (!v || !W || !y || (!R && p->nkz > 0)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_fwd: NULL data pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* vhat = vhat_save ? static_cast<float2*>(vhat_save) : wsp<float2>(p, p->o_vhat);
+  FNO_TRY(spectral_fwd_to_slab(p, v, static_cast<const float2*>(R), vhat, st));
+  return stage_c_fwd(p, v, W, b, y, z_save, st);
+}
+
 static fno_status xy_layer_bwd(fno_plan_t p, const float* v, const float* z_saved, const void* vhat_saved,
-                                    const float* dy, const void* R, const float* W, float* dv, void* dR, float* dW,
-                                    float* db, int accumulate, void* stream) {
+                               const float* dy, const void* R, const float* W, float* dv, void* dR, float* dW,
+                               float* db, int accumulate, void* stream) {
   FNO_TRY(check_ready(p, "fno_layer_bwd"));
+  FNO_TRY(not_grouped(p, "fno_layer_bwd"));
   p->dir = 1;
   if (!v || !dy || !W || !dv || !dW || (!R && p->nkz > 0) || (p->act_gelu && !z_saved))
     return fail(FNO_ERR_INVALID_ARGUMENT, "fno_layer_bwd: NULL data pointer (v, dy, W, dv, dW, R and z_saved for GELU are required)");
@@ -785,20 +934,139 @@ static fno_status xy_layer_bwd(fno_plan_t p, const float* v, const float* z_save
   const int mode = p->act_gelu ? MODE_DZ_GELU : MODE_DZ_NONE;
   FNO_TRY(spectral_bwd_to_slab(p, dy, z_saved, mode, static_cast<const float2*>(R), static_cast<const float2*>(vhat_saved),
                                static_cast<float2*>(dR), accumulate, st));
-  PassCParams c = make_c(p, EPI_BWD);
-  c.v = v; c.dy = p->act_gelu ? wsp<float>(p, p->o_dz) : dy; c.W = W; c.out = dv;   // dz formed by pass A
-  c.dWpart = wsp<float>(p, p->o_dwpart);
-  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st), "pass C (layer backward)");
+  const float* dz = p->act_gelu ? wsp<float>(p, p->o_dz) : dy;   // dz formed by pass A
+  if (p->P == 1) return stage_c_bwd(p, v, dz, W, dv, nullptr, dW, db, accumulate, st);
+  float* loc = wsp<float>(p, p->o_dwloc);
+  float* all = wsp<float>(p, p->o_dwall);
+  FNO_TRY(stage_c_bwd(p, v, dz, W, dv, loc, nullptr, nullptr, 0, st));
   const int len = p->C * p->C + p->C;
-  if (p->P == 1) {
-    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, p->grid_c_bwd, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
-  } else {
-    float* loc = wsp<float>(p, p->o_dwloc);
-    float* all = wsp<float>(p, p->o_dwall);
-    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, p->grid_c_bwd, len, len, loc, nullptr, 0, st), "dW/db local reduction");
-    FNO_NCCL(ncclAllGather(loc, all, size_t(len), ncclFloat, p->comm->nccl, st), "dW/db all-gather");
-    FNO_LAUNCH(p, ST_DW, launch_rowsum(all, p->P, len, p->C * p->C, dW, db, accumulate, st), "dW/db rank-ordered sum");
+  FNO_NCCL(ncclAllGather(loc, all, size_t(len), ncclFloat, p->comm->nccl, st), "dW/db all-gather");
+  FNO_LAUNCH(p, ST_DW, launch_rowsum(all, p->P, len, p->C * p->C, dW, db, accumulate, st), "dW/db rank-ordered sum");
+  return FNO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plan groups: the P ranks of a decomposition as P plans in ONE process on ONE
+// device (fno_group_*).  The data path is the decomposed one -- every rank's
+// x/y box, the send-ready slab chunks stored straight into the owners' buffers
+// (the peer-store exchange, with same-device pointers), kz-owned weights and
+// the rank-ordered dW / db sum -- with each stage run for every rank before the
+// next stage, so no rank ever waits for another (stream order is the barrier).
+// ---------------------------------------------------------------------------
+namespace {
+
+bool same_problem(const fno_problem& a, const fno_problem& b) {
+  for (int d = 0; d < 4; ++d)
+    if (a.grid[d] != b.grid[d] || a.modes[d] != b.modes[d]) return false;
+  return a.batch == b.batch && a.width == b.width && a.pgrid[0] == b.pgrid[0] && a.pgrid[1] == b.pgrid[1] &&
+         a.flags == b.flags;
+}
+
+fno_status check_group(int n, fno_plan_t const* plans, const char* who) {
+  if (n < 1 || !plans) return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": need n >= 1 plans");
+  for (int r = 0; r < n; ++r) {
+    fno_plan_t p = plans[r];
+    if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, std::string(who) + ": NULL plan");
+    if (!p->group || p->P != n || p->rank != r)
+      return fail(FNO_ERR_INVALID_STATE, std::string(who) + ": plans must be a connected group in rank order (fno_group_connect)");
   }
+  return FNO_OK;
+}
+
+}  // namespace
+
+extern "C" fno_status fno_group_connect(int n, fno_plan_t* plans) {
+  if (n < 1 || n > FNO_MAXP || !plans) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_connect: need 1 <= n <= 64 plans");
+  int dev0 = -1;
+  for (int r = 0; r < n; ++r) {
+    fno_plan_t p = plans[r];
+    if (!p) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_connect: NULL plan");
+    if (p->P != n || p->rank != r) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_connect: plan r must be rank r of an n-rank problem");
+    if (!same_problem(p->pb, plans[0]->pb)) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_connect: plans of different problems");
+    if (!p->ws) return fail(FNO_ERR_INVALID_STATE, "fno_group_connect: workspace not set");
+    if (p->peer || p->io_on) return fail(FNO_ERR_INVALID_STATE, "fno_group_connect: plan already connected or io-partitioned");
+    cudaPointerAttributes at{};
+    FNO_CUDA(cudaPointerGetAttributes(&at, p->ws), "fno_group_connect: workspace attributes");
+    if (at.type != cudaMemoryTypeDevice) return fail(FNO_ERR_WORKSPACE, "fno_group_connect: workspace is not device memory");
+    if (dev0 < 0) dev0 = at.device;
+    if (at.device != dev0) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_connect: all workspaces must be on one device");
+  }
+  std::vector<char*> bases(n);
+  for (int r = 0; r < n; ++r) bases[r] = static_cast<char*>(plans[r]->ws);
+  for (int r = 0; r < n; ++r) {
+    plans[r]->peer_ws = bases;
+    plans[r]->peer = n > 1 ? 1 : 0;
+    plans[r]->group = 1;
+  }
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_group_spectral_conv_fwd(int n, fno_plan_t* plans, const float* const* v, const void* const* R,
+                                                  float* const* u, void* const* vhat_save, void* stream) {
+  FNO_TRY(check_group(n, plans, "fno_group_spectral_conv_fwd"));
+  if (!v || !R || !u) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_spectral_conv_fwd: NULL array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto vh = [&](int r) { return vhat_save && vhat_save[r] ? static_cast<float2*>(vhat_save[r]) : wsp<float2>(plans[r], plans[r]->o_vhat); };
+  for (int r = 0; r < n; ++r) { plans[r]->dir = 0; FNO_TRY(sf_stage_a(plans[r], v[r], st)); }
+  for (int r = 0; r < n; ++r) FNO_TRY(sf_stage_b(plans[r], static_cast<const float2*>(R[r]), vh(r), st));
+  for (int r = 0; r < n; ++r) FNO_TRY(stage_c_u(plans[r], u[r], st));
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_group_spectral_conv_bwd(int n, fno_plan_t* plans, const float* const* g, const void* const* R,
+                                                  const void* const* vhat_saved, float* const* dv, void* const* dR,
+                                                  int accumulate, void* stream) {
+  FNO_TRY(check_group(n, plans, "fno_group_spectral_conv_bwd"));
+  if (!g || !R) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_spectral_conv_bwd: NULL array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int r = 0; r < n; ++r) { plans[r]->dir = 1; FNO_TRY(sb_stage_a(plans[r], g[r], nullptr, MODE_V, st)); }
+  for (int r = 0; r < n; ++r)
+    FNO_TRY(sb_stage_b(plans[r], static_cast<const float2*>(R[r]), vhat_saved ? static_cast<const float2*>(vhat_saved[r]) : nullptr,
+                       dR ? static_cast<float2*>(dR[r]) : nullptr, accumulate, st));
+  if (dv)
+    for (int r = 0; r < n; ++r) FNO_TRY(stage_c_u(plans[r], dv[r], st));
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_group_layer_fwd(int n, fno_plan_t* plans, const float* const* v, const void* const* R,
+                                          const float* W, const float* b, float* const* y, float* const* z_save,
+                                          void* const* vhat_save, void* stream) {
+  FNO_TRY(check_group(n, plans, "fno_group_layer_fwd"));
+  if (!v || !R || !W || !y) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_layer_fwd: NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto vh = [&](int r) { return vhat_save && vhat_save[r] ? static_cast<float2*>(vhat_save[r]) : wsp<float2>(plans[r], plans[r]->o_vhat); };
+  for (int r = 0; r < n; ++r) { plans[r]->dir = 0; FNO_TRY(sf_stage_a(plans[r], v[r], st)); }
+  for (int r = 0; r < n; ++r) FNO_TRY(sf_stage_b(plans[r], static_cast<const float2*>(R[r]), vh(r), st));
+  for (int r = 0; r < n; ++r) FNO_TRY(stage_c_fwd(plans[r], v[r], W, b, y[r], z_save ? z_save[r] : nullptr, st));
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_group_layer_bwd(int n, fno_plan_t* plans, const float* const* v, const float* const* z_saved,
+                                          const void* const* vhat_saved, const float* const* dy, const void* const* R,
+                                          const float* W, float* const* dv, void* const* dR, float* dW, float* db,
+                                          int accumulate, void* stream) {
+  FNO_TRY(check_group(n, plans, "fno_group_layer_bwd"));
+  const int act = plans[0]->act_gelu;
+  if (!v || !dy || !R || !W || !dv || !dW || !vhat_saved || (act && !z_saved))
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_group_layer_bwd: NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int mode = act ? MODE_DZ_GELU : MODE_DZ_NONE;
+  for (int r = 0; r < n; ++r) { plans[r]->dir = 1; FNO_TRY(sb_stage_a(plans[r], dy[r], act ? z_saved[r] : nullptr, mode, st)); }
+  for (int r = 0; r < n; ++r)
+    FNO_TRY(sb_stage_b(plans[r], static_cast<const float2*>(R[r]), static_cast<const float2*>(vhat_saved[r]),
+                       dR ? static_cast<float2*>(dR[r]) : nullptr, accumulate, st));
+  const int len = plans[0]->C * plans[0]->C + plans[0]->C;
+  float* all = wsp<float>(plans[0], plans[0]->o_dwall);
+  for (int r = 0; r < n; ++r) {
+    fno_plan_t p = plans[r];
+    const float* dz = act ? wsp<float>(p, p->o_dz) : dy[r];
+    float* loc = wsp<float>(p, p->o_dwloc);
+    FNO_TRY(stage_c_bwd(p, v[r], dz, W, dv[r], loc, nullptr, nullptr, 0, st));
+    FNO_CUDA(cudaMemcpyAsync(all + size_t(r) * len, loc, size_t(len) * sizeof(float), cudaMemcpyDeviceToDevice, st),
+             "group: dW/db gather");
+  }
+  FNO_LAUNCH(plans[0], ST_DW, launch_rowsum(all, n, len, plans[0]->C * plans[0]->C, dW, db, accumulate, st),
+             "group: dW/db rank-ordered sum");
   return FNO_OK;
 }
 
@@ -821,6 +1089,7 @@ extern "C" fno_status fno_plan_set_io_partition(fno_plan_t p, const int32_t io_p
   if (!p || !io_pgrid) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_io_partition: NULL argument");
   if (p->ws) return fail(FNO_ERR_INVALID_STATE, "fno_plan_set_io_partition: call before fno_plan_set_workspace");
   if (p->io_on) return fail(FNO_ERR_INVALID_STATE, "fno_plan_set_io_partition: already set");
+  if (p->peer) return fail(FNO_ERR_INVALID_STATE, "fno_plan_set_io_partition: call before fno_plan_connect_peers");
   const long long ext[4] = {p->X, p->Y, p->Z, p->T};
   long long prod = 1;
   for (int d = 0; d < 4; ++d) {

@@ -17,6 +17,15 @@
 
 #define FNO_MAXP 64
 
+// Profiling-only ablation switches (PassCParams::ablate), compiled in only by
+// the scripts/ablate*.sh builds (-DFNO_ABLATE_BUILD); in the product library
+// every ablation branch folds away at compile time.
+#ifdef FNO_ABLATE_BUILD
+#define FNO_ABL(p, bit) (((p).ablate & (bit)) != 0)
+#else
+#define FNO_ABL(p, bit) false
+#endif
+
 namespace fno {
 
 // ---------------------------------------------------------------------------
@@ -146,14 +155,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned phase) {
       : "memory");
   return ok != 0;
 }
-// bounded wait: a barrier that never completes (a malformed async copy or MMA)
-// traps the kernel instead of hanging the GPU.  Each try_wait may suspend the
-// warp in hardware (time hint 10 ms) until the phase completes, so waiting
-// warps do not spin on the issue slots the working warps need.
+// bounded wait: a barrier that never completes (a malformed async copy or MMA,
+// a protocol bug) traps the kernel after ~4 s instead of hanging the GPU.  Each
+// try_wait may suspend the warp in hardware (time hint 10 ms) until the phase
+// completes, so waiting warps do not spin on the issue slots the working
+// warps need; the deadline is checked on the global nanosecond timer.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  unsigned spins = 0;
+  if (mbar_try_wait(bar, phase)) return;
+  const unsigned long long t0 = global_ns();
   while (!mbar_try_wait(bar, phase)) {
-    if (++spins > (1u << 22)) __trap();
+    if (global_ns() - t0 > 4000000000ull) __trap();
   }
 }
 

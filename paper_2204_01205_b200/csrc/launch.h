@@ -48,6 +48,14 @@ cudaError_t launch_pass_c2(const PassCParams& p, int LZ, int LT, int CP, int mod
 bool pass_c3_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CP, int* TCH, size_t* smem);
 cudaError_t launch_pass_c3(const PassCParams& p, int LZ, int LT, int CP, int grid, size_t smem, cudaStream_t st);
 
+// pass C generation 4 (pass_c4.cu): warp-specialised, TMA input ring, tcgen05
+// 1x1 (fwd), W^T dz and dW / db (bwd); every epilogue mode.  false if the
+// configuration is not covered; launch returns cudaErrorNotSupported when the
+// tensors' alignment rules out the TMA tile view (the caller falls back)
+bool pass_c4_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CP, int* NS, size_t* smem);
+cudaError_t launch_pass_c4(const PassCParams& p, int LZ, int LT, int CP, int mode, int grid, size_t smem,
+                           cudaStream_t st);
+
 // pass B: y forward (slab -> H), x forward (H -> V^), x inverse (W^ -> H'),
 // y inverse (H' -> slab)
 cudaError_t launch_b_yfwd(const PassBParams& p, int L, cudaStream_t st);

@@ -22,8 +22,12 @@ bool pass_c2_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   // with two buffers, then the largest that fits one CTA
   int tmax = (T + 3) & ~3;
   if (tmax * LZ > C2T) tmax = (C2T / LZ) & ~3;
+#ifdef FNO_DEV_KNOBS   // development builds only (scripts/variant_lib.sh): force the X buffer count
   const char* nxe = std::getenv("FNO_PASS_C_NX");
   const int force_nx = nxe ? std::atoi(nxe) : 0;
+#else
+  const int force_nx = 0;
+#endif
   // full: only the largest t chunk (a whole 128-point tile).  The backward keeps
   // two buffers while two CTAs per SM fit at full tiles, else takes one buffer at
   // full tiles (c4: 3.49 vs 5.03 ms/launch with two buffers at half tiles)

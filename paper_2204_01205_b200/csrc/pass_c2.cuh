@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
     // ---- phase 1: inverse t (C2R weights folded in), items (c, kz', rt) ----
     // The +kz' and -kz' rows of the slab (L2-resident) are folded into one
     // complex row whose inverse t-DFT is the real z-transform's input.
-    for (int it = (p.ablate & 16) ? C * nk * p.Qt : tid; it < C * nk * p.Qt; it += C2T) {
+    for (int it = FNO_ABL(p, 16) ? C * nk * p.Qt : tid; it < C * nk * p.Qt; it += C2T) {
       const int rt = it % p.Qt;
       const int pid = it / p.Qt;
       const int c = pid / nk, kzp = pid - c * nk;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
         }
       }
       // ---- phase 2: inverse z (real output), items (c, tt) -> U ----------
-      for (int it = (p.ablate & 1) ? C * tcw : tid; it < C * tcw; it += C2T) {
+      for (int it = FNO_ABL(p, 1) ? C * tcw : tid; it < C * tcw; it += C2T) {
         const int c = it / tcw, tt = ta + (it - c * tcw);
         float2 e[LZ];
 #pragma unroll
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
         for (int s = 0; s < LZ; ++s) uo[s * TCH] = y[s].x * p.inv_n;
       }
       // ---- bwd: dW / db on this tile (X only; no barrier after phase 2) ----
-      if (EPI == EPI_BWD && !(p.ablate & 8)) {
+      if (EPI == EPI_BWD && !FNO_ABL(p, 8)) {
         const float* Dz = X + ob * DB * XPS;
         const float* Vv = X + CP * XPS + ib * DB * XPS;
         for (int q = lane; q < NQ; q += 32) {
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
       float4 acc[Q4];
 #pragma unroll
       for (int j = 0; j < Q4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (item1 && !(p.ablate & 2)) {
+      if (item1 && !FNO_ABL(p, 2)) {
         const float* wq = Ws + qtr1 * QW;
 #pragma unroll
         for (int k = 0; k < CP; ++k) {
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
       }
       // ---- epilogue: + u (+ b, GELU), stores -------------------------------
       const int k0 = RAG ? max(0, ta - tq1) : 0, k1 = RAG ? min(4, tb - tq1) : 4;   // valid points of this thread's quad
-      if (item1 && k0 < k1 && !(p.ablate & 4)) {
+      if (item1 && k0 < k1 && !FNO_ABL(p, 4)) {
         const long long gs = cbase + rz * T + t0 + go1;
         // TMA tiles start 16-byte aligned in memory (c2_tile_group), so do their full quads
         const bool full4 = !RAG || ((vec_out || tma) && k0 == 0 && k1 == 4);

@@ -20,8 +20,10 @@ cudaError_t launch_pass_c3_cp20(const C2Maps&, const PassCParams&, int LZ, int L
 // multiple of TCH and of 4 (TMA tile loads); FNO_PASS_C3=0 disables
 bool pass_c3_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* TCH, size_t* smem) {
   if (mode != EPI_FWD) return false;
+#ifdef FNO_DEV_KNOBS   // development builds only: FNO_PASS_C3=0 selects the FFMA pass_c2
   const char* e = std::getenv("FNO_PASS_C3");
   if (e && e[0] == '0') return false;
+#endif
   const int CP = (C + 3) & ~3;
   if (CP > 20) return false;
   if (LZ != 8 && LZ != 16 && LZ != 32) return false;

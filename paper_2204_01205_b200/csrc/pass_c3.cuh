@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
       const long long col_next = col + gridDim.x;
       group_sync(1, NTT);   // previous column's phase 2 done with Bb
       // ---- phase 1: inverse t (C2R weights and 1/N folded in), items (c, kz', rt)
-      for (int it = (p.ablate & 16) ? C * nk * p.Qt : ttid; it < C * nk * p.Qt; it += NTT) {
+      for (int it = FNO_ABL(p, 16) ? C * nk * p.Qt : ttid; it < C * nk * p.Qt; it += NTT) {
         const int rt = it % p.Qt;
         const int pid = it / p.Qt;
         const int c = pid / nk, kzp = pid - c * nk;
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
           cp_wait<0>();
           group_sync(1, NTT);
         }
-        for (int e = (p.ablate & 2) ? C3T * (CP / 4) : ttid; e < C3T * (CP / 4); e += NTT) {
+        for (int e = FNO_ABL(p, 2) ? C3T * (CP / 4) : ttid; e < C3T * (CP / 4); e += NTT) {
           const int g = e / C3T, pp = e - g * C3T;
           float4 hi, lo;
           const float x0 = X[(4 * g + 0) * C3T + pp], x1 = X[(4 * g + 1) * C3T + pp];
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
         // ---- phase 2: inverse z (real output), items (c, tt) -> U[b] --------
         const int ta = RAG ? max(0, -t0) : 0, tb = RAG ? min(TCH, T - t0) : TCH;   // valid columns; the others are never stored
-        for (int it = (p.ablate & 1) ? C * TCH : ttid; it < C * TCH; it += NTT) {
+        for (int it = FNO_ABL(p, 1) ? C * TCH : ttid; it < C * TCH; it += NTT) {
           const int c = it / TCH, tt = it - c * TCH;
           if (tt < ta || tt >= tb) continue;
           float2 e[LZ];
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
         tc_fence_before();
 #pragma unroll
         for (int o = 0; o < CP; ++o) {
-          if (o >= C || (p.ablate & 4)) break;
+          if (o >= C || FNO_ABL(p, 4)) break;
           U[o * UPS + tid] += __uint_as_float(d[o >> 3][o & 7]);
         }
         __syncwarp();
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
 #pragma unroll
         for (int j = 0; j < (CP + 3) / 4; ++j) {
           const int o = (lane >> 3) + 4 * j;
-          if (o >= C || (p.ablate & 4) || k0 >= k1) break;
+          if (o >= C || FNO_ABL(p, 4) || k0 >= k1) break;
           float4 r = *reinterpret_cast<const float4*>(U + o * UPS + pq);
           const long long g = gq + o * chan_stride;
           if (v4) {

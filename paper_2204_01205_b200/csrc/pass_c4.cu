@@ -1,0 +1,82 @@
+// Host side of pass C generation 4 (kernel: pass_c4.cuh; one translation unit
+// per padded width CP so the instantiations compile in parallel): eligibility,
+// ring depth, shared-memory size and the TMA tensor maps of the tile inputs.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "pass_c4.cuh"
+
+namespace fno {
+
+// padded channel width of the pass_c4 instantiations
+static int c4_cp_of(int C) {
+  if (C <= 20) return (C + 3) & ~3;
+  if (C <= 24) return 24;
+  if (C <= 32) return 32;
+  return 0;
+}
+
+// Tiles of exactly 128 points (LZ in {8, 16, 32}, TCH = 128 / LZ <= T); the
+// deepest input ring that fits 227 KB (forward up to 6 stages, backward up to
+// 4; at least 2, else the plan keeps pass_c2 / pass_c3)
+bool pass_c4_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* NS, size_t* smem) {
+  (void)mt;
+  const int CP = c4_cp_of(C);
+  if (!CP) return false;
+  if (LZ != 8 && LZ != 16 && LZ != 32) return false;
+  if (128 / LZ > T) return false;
+  const size_t cap = 227 * 1024;
+  if (mode == EPI_U) {
+    const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, 1).total;
+    if (s > cap) return false;
+    *CPo = CP; *NS = 1; *smem = s;
+    return true;
+  }
+  for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= 2; --ns) {
+    const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, ns).total;
+    if (s <= cap) {
+      *CPo = CP; *NS = ns; *smem = s;
+      return true;
+    }
+  }
+  return false;
+}
+
+cudaError_t launch_pass_c4(const PassCParams& p0, int LZ, int LT, int CP, int mode, int grid, size_t smem,
+                           cudaStream_t st) {
+  PassCParams p = p0;
+  p.TCH = 128 / LZ;
+  C2Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  // one tile geometry for inputs and outputs (16-byte aligned TMA boxes and
+  // float4 stores; the row-group view when T % 4 != 0)
+  p.tma_g = c2_tile_group(p, LZ, p.out);
+  if (p.tma_g <= 0) return cudaErrorNotSupported;
+  if (mode != EPI_U) {
+    const float* src0 = mode == EPI_FWD ? p.v : p.dy;
+    if (c2_tile_group(p, LZ, src0) != p.tma_g || !c2_encode_tile_map(&maps.m[0], src0, p, LZ))
+      return cudaErrorNotSupported;
+    if (mode == EPI_BWD && (c2_tile_group(p, LZ, p.v) != p.tma_g || !c2_encode_tile_map(&maps.m[1], p.v, p, LZ)))
+      return cudaErrorNotSupported;
+    if (p.zsave && c2_tile_group(p, LZ, p.zsave) != p.tma_g) return cudaErrorNotSupported;
+  }
+#define FNO_C4_CP(cp)                                                                        \
+  case cp:                                                                                   \
+    return mode == EPI_FWD   ? launch_pass_c4_cp##cp##_fwd(maps, p, LZ, LT, grid, smem, st)  \
+           : mode == EPI_BWD ? launch_pass_c4_cp##cp##_bwd(maps, p, LZ, LT, grid, smem, st)  \
+                             : launch_pass_c4_cp##cp##_u(maps, p, LZ, LT, grid, smem, st);
+  switch (CP) {
+    FNO_C4_CP(4)
+    FNO_C4_CP(8)
+    FNO_C4_CP(12)
+    FNO_C4_CP(16)
+    FNO_C4_CP(20)
+    FNO_C4_CP(24)
+    FNO_C4_CP(32)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FNO_C4_CP
+}
+
+}  // namespace fno

@@ -34,6 +34,8 @@ def stage_of(name):
         return {"1": "fwd.pass_c", "2": "bwd.pass_c"}.get(targs[3], base)
     if base == "pass_c3_fwd_kernel":                                         # tcgen05 1x1 forward
         return "fwd.pass_c"
+    if base == "pass_c4_kernel" and len(targs) >= 4:                          # <LZ, LT, CP, EPI, HALF, RAG>
+        return {"0": "pass_c_u", "1": "fwd.pass_c", "2": "bwd.pass_c"}.get(targs[3], base)
     if base == "mix_fwd_kernel":
         return "fwd.mix"
     if base == "mix_bwd_kernel":

@@ -217,17 +217,13 @@ def test_full_size_c3_c4_forward_sampled_outputs(ci):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.slow
-def test_full_size_c2_backward():
-    """The c2 backward at full size (the launch configuration bench.py times):
-    the oracle forms z, dz on the whole grid, then dR, dW, db in full and dv at
-    512 sampled points (dv = W^T dz + S^T dz with S^T by R^H, reading of P:74)."""
+def _backward_vs_oracle(grid, C, modes, pr, seed_pts, n_pts=512):
+    """Layer fwd + bwd through libfno on pr's inputs; the oracle forms z, dz on
+    the whole grid, then dR, dW, db in full and dv at n_pts sampled points
+    (dv = W^T dz + S^T dz with S^T by R^H, reading of P:74)."""
     import torch
     from tests import _gpu as G
     import paper_2204_01205_b200 as fno
-    cfg = synth.CONFIGS[2]
-    grid, C, modes = cfg["grid"], cfg["width"], cfg["modes"]
-    pr = synth.problem(2, with_dy=True)
     plan = G.make_plan(grid, C, modes)
     vt, Rt, Wt, bt = G.t32(pr["v"]), G.tc64(pr["R"]), G.t32(pr["W"]), G.t32(pr["b"])
     y = torch.empty_like(vt)
@@ -250,16 +246,84 @@ def test_full_size_c2_backward():
     X, Y, Z, T = grid
     cw = sp.c_weight(T, modes[3])
     dR_ref = np.einsum("bixyzt,boxyzt->ioxyzt", np.conj(vh_ref), gh) * (cw / float(X * Y * Z * T))
-    assert rel_l2(G.np64(dR), dR_ref) < TOL
-    dW_ref = np.einsum("boxyzt,bixyzt->oi", dz, v64)
-    assert rel_l2(G.np64(dW), dW_ref) < TOL
-    assert rel_l2(G.np64(db), dz.sum(axis=(0, 2, 3, 4, 5))) < TOL
+    errs = {"dR": rel_l2(G.np64(dR), dR_ref)}
+    errs["dW"] = rel_l2(G.np64(dW), np.einsum("boxyzt,bixyzt->oi", dz, v64))
+    errs["db"] = rel_l2(G.np64(db), dz.sum(axis=(0, 2, 3, 4, 5)))
     RH = np.conj(np.swapaxes(R64, 0, 1))
     wh = sp.mix(gh, RH)
-    rng = np.random.default_rng(11)
-    pts = np.stack([rng.integers(0, n, size=512) for n in grid], -1)
+    rng = np.random.default_rng(seed_pts)
+    pts = np.stack([rng.integers(0, n, size=n_pts) for n in grid], -1)
     sel = (slice(None), pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3])          # [C, P] of batch 0
     dv_ref = W64.T @ dz[0][sel] + sp.inverse_modes_at(wh, grid, pts)[0]
-    assert rel_l2(G.np64(dv)[0][sel], dv_ref) < TOL
+    errs["dv"] = rel_l2(G.np64(dv)[0][sel], dv_ref)
     del dv, dR
     torch.cuda.empty_cache()
+    bad = {k: e for k, e in errs.items() if not e < TOL}
+    assert not bad, errs
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ci", [2, 3], ids=["c2", "c3"])
+def test_full_size_backward(ci):
+    """BASELINE configs[1] (c2) and configs[2] (c3, the metric's training-step
+    shape: 64^3 x 30, width 20, modes 12) backward at full size, in the launch
+    configuration bench.py times."""
+    cfg = synth.CONFIGS[ci]
+    _backward_vs_oracle(cfg["grid"], cfg["width"], cfg["modes"], synth.problem(ci, with_dy=True), seed_pts=11 + ci)
+
+
+# Width-20 backward instantiations of the other configs.  The pass-C kernels
+# are specialised on (LZ, LT, CP) -- fixed by Z, T, modes and C -- and launched
+# on min(columns, 2 x 148) persistent CTAs; with >= 1024 x/y columns the launch
+# (grid, shared memory, tile buffers) equals the full-size one, so these x/y-
+# reduced boxes run exactly the c4 / c5 kernels and launch configurations at a
+# size the fp64 oracle affords in full.  Plus the odd-T ragged-tile path
+# (T = 15: the 4-row TMA group view, tma_g = 4).
+INSTANCES = [
+    ("c4_box", (32, 32, 128, 32), 20, (12, 12, 12, 12), "ns"),     # c4: LZ 16, LT 32, CP 20
+    ("c5_box", (32, 32, 256, 32), 20, (16, 16, 16, 16), "ns"),     # c5: LZ 32, LT 32, CP 20
+    ("oddT", (32, 32, 32, 15), 20, (8, 8, 8, 6), "co2"),           # T odd: tma_g = 4, ragged chunks
+    ("oddT_c8", (16, 32, 64, 15), 8, (6, 6, 12, 8), "ns"),         # T odd, LT = 15, CP 8
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("inst", INSTANCES, ids=lambda c: c[0])
+def test_width20_instantiations_fwd_bwd(inst):
+    from tests import _gpu as G
+    name, grid, C, modes, shape = inst
+    v = synth.field((1, C) + grid, modes, 1234, shape)
+    R = synth.spectral_weights(C, C, modes, 1235)
+    W, b = synth.channel_weights(C, 1236)
+    dy = synth.cotangent(v.shape, 1237)
+    plan = G.make_plan(grid, C, modes)
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    y_ref, z_ref = sp.layer_fwd(G.f32(v), G.f32(R), G.f32(W), G.f32(b), modes)
+    assert rel_l2(G.np64(z), z_ref) < TOL
+    assert rel_l2(G.np64(y), y_ref) < TOL
+    _backward_vs_oracle(grid, C, modes, dict(v=v, R=R, W=W, b=b, dy=dy), seed_pts=5)
+
+
+@pytest.mark.parametrize("C", [24, 32], ids=["C24", "C32"])
+def test_wide_channels_fwd_bwd(C):
+    """Widths above 20 (the network accepts C <= 32): layer forward and backward
+    vs the oracle."""
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    grid, modes = (16, 16, 32, 16), (4, 4, 6, 6)
+    v, R, W, b, dy = _problem(grid, C, modes, 1, seed=606)
+    plan = G.make_plan(grid, C, modes)
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    y_ref, z_ref = sp.layer_fwd(G.f32(v), G.f32(R), G.f32(W), G.f32(b), modes)
+    assert rel_l2(G.np64(y), y_ref) < TOL
+    dyt = G.t32(dy)
+    dv = torch.empty_like(dyt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.empty((C, C), device="cuda")
+    db = torch.empty((C,), device="cuda")
+    fno.layer_bwd(plan, G.t32(v), z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db)
+    torch.cuda.synchronize()
+    dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
+    for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
+        assert rel_l2(G.np64(got), ref) < TOL, name
