@@ -734,6 +734,7 @@ def main():
                     help="time the whole network's training step (lift, blocks, projection, loss, backward, Adam)")
     ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c3",
                     help="BASELINE.json workload (default c3 = configs[2], strong; c2 configs[1]; c4 weak; c5 strong)")
+    ap.add_argument("--allow-dev", action="store_true", help="allow FNO_LIB / FNO_ABLATE development builds (A/B only)")
     ap.add_argument("--no-phases", action="store_true", help="skip the per-phase (fwd inference / fwd train / bwd) timing")
     args = ap.parse_args()
     global CONFIG_INDEX
@@ -749,8 +750,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if os.environ.get("FNO_ABLATE") or os.environ.get("FNO_LIB"):
-        raise SystemExit("bench.py: FNO_ABLATE / FNO_LIB select profiling-only builds; unset them for a bench line")
+    if (os.environ.get("FNO_ABLATE") or os.environ.get("FNO_LIB")) and not args.allow_dev:
+        raise SystemExit("bench.py: FNO_ABLATE / FNO_LIB select development builds; unset them for a bench line "
+                         "(--allow-dev for A/B runs; the FNO_* environment is recorded in config.env)")
     if world not in PGRIDS:
         raise SystemExit(f"unsupported world size {world} (1, 2, 4, 8)")
     if world > 1:

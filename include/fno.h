@@ -133,6 +133,11 @@ fno_status fno_plan_connect_peers(fno_plan_t plan, void* stream);
  * 1 = the generic pass_c.  The family-4 launch falls back to the next family
  * when the tensors' alignment rules out its TMA view. */
 fno_status fno_plan_pass_c_info(fno_plan_t plan, int mode, int64_t info[4]);
+/* Selects the pass C kernel family (as in fno_plan_pass_c_info) for mode 0
+ * (spectral u), 1 (layer forward) or 2 (layer backward).  fno_plan_create
+ * picks the measured-fastest eligible family; this call is for A/B runs and
+ * tests.  FNO_ERR_PLAN if the family does not cover the problem. */
+fno_status fno_plan_set_pass_c(fno_plan_t plan, int mode, int family);
 /* *enabled = 1 if fno_plan_connect_peers switched the exchanges to peer stores. */
 fno_status fno_plan_peer_enabled(fno_plan_t plan, int* enabled);
 /* Caller-side partition of the fields (the paper's App. A 3-D

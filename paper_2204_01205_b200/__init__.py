@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
             "fno_plan_connect_peers": [vp, vp],
             "fno_plan_peer_enabled": [vp, P(i32)],
             "fno_plan_pass_c_info": [vp, i32, P(ctypes.c_int64)],
+            "fno_plan_set_pass_c": [vp, i32, i32],
             "fno_plan_local_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
             "fno_plan_set_io_partition": [vp, P(ctypes.c_int32)],
             "fno_plan_io_box": [vp, P(ctypes.c_int64), P(ctypes.c_int64)],
@@ -344,8 +345,18 @@ def plan_pass_c_kernels(plan: Plan) -> dict:
     for m, name in enumerate(("u", "fwd", "bwd")):
         info = (ctypes.c_int64 * 4)()
         _check(lib().fno_plan_pass_c_info(plan.handle, m, info), "fno_plan_pass_c_info")
-        out[name] = {"family": fam.get(info[0], info[0]), "width": info[1], "stages": info[2], "smem": info[3]}
+        out[name] = {"family": fam.get(info[0], info[0]), "width": info[1], "stages": info[2] & 255,
+                     "smem": info[3]}
+        if info[0] == 4 and info[2] >> 8:
+            out[name]["u_buffers"] = info[2] >> 8
     return out
+
+
+def plan_set_pass_c(plan: Plan, mode: str, family: int):
+    """Force the pass C kernel family (1 pass_c, 2 pass_c2, 3 pass_c3, 4 pass_c4) for mode "u" / "fwd" / "bwd"
+    (A/B runs and tests; the plan's default is the measured-fastest eligible family)."""
+    m = {"u": 0, "fwd": 1, "bwd": 2}[mode]
+    _check(lib().fno_plan_set_pass_c(plan.handle, m, int(family)), "fno_plan_set_pass_c")
 
 
 def kernel_launches() -> int:

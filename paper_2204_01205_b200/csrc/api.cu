@@ -63,8 +63,6 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-static const bool kC4Layer = false;   // pass_c4 for the layer forward / backward
-
 enum Stage { ST_PASS_A, ST_EX1, ST_B_YF, ST_B_XF, ST_MIX, ST_B_XI, ST_B_YI, ST_EX2, ST_PASS_C, ST_DW, ST_N };
 static const char* kStageNames[2 * ST_N] = {
     "fwd.pass_a", "fwd.exchange_1", "fwd.b_y_fwd", "fwd.b_x_fwd", "fwd.mix", "fwd.b_x_inv", "fwd.b_y_inv", "fwd.exchange_2", "fwd.pass_c", "fwd.unused",
@@ -96,17 +94,17 @@ struct fno_plan_s {
   int LZ, LT, LX, LY;
   int Qz, Qt, Qx, Qy;
   int num_sms = 148;
-  int grid_c = 1, grid_c_bwd = 1, grid_c_u = 1;
-  size_t smem_a[3] = {0, 0, 0}, smem_c_u = 0, smem_c_fwd = 0, smem_c_bwd = 0;
+  size_t smem_a[3] = {0, 0, 0};
   int np_a[3] = {1, 1, 1}, ns_a[3] = {2, 2, 2}, tma_a = 0, grid_a_m[3] = {1, 1, 1};
-  int tch[3] = {0, 0, 0}, vw[3] = {1, 1, 1};  // pass C tile config per EPI mode
-  int c2cp[3] = {0, 0, 0};                     // > 0: pass_c2 kernel with that padded width
-  int c2nx[3] = {2, 2, 2};                     // pass_c2 X tile buffers
-  int c3cp[3] = {0, 0, 0};                     // > 0: tensor-core pass_c3 kernel with that padded width
-  int c4cp[3] = {0, 0, 0};                     // > 0: warp-specialised pass_c4 kernel (preferred)
-  int c4ns[3] = {0, 0, 0};                     // its input-ring depth
-  size_t c4smem[3] = {0, 0, 0};
-  int c4grid = 1;                              // one CTA per SM
+  // pass C kernel families per epilogue mode (EPI_U, EPI_FWD, EPI_BWD): index
+  // family - 1 (1 generic pass_c, 2 pass_c2 FFMA, 3 pass_c3 tcgen05 1x1,
+  // 4 pass_c4 warp-specialised tcgen05); cp == 0: not eligible
+  struct KCfg {
+    int cp = 0, tch = 0, vw = 1, nx = 0, grid = 1;
+    size_t smem = 0;
+  };
+  KCfg kc[4][3];
+  int fam[3] = {1, 1, 1};                      // the family each mode launches (fno_plan_set_pass_c)
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -326,48 +324,48 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
 
   // pass A batching (planes per TMA batch) per input mode
   for (int m = 0; m < 3; ++m) pass_a_config(int(p->Z), int(p->T), p->mz, m, &p->np_a[m], &p->ns_a[m], &p->smem_a[m], &p->tma_a);
-  pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_U, &p->tch[0], &p->vw[0], &p->smem_c_u);
-  pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &p->tch[1], &p->vw[1], &p->smem_c_fwd);
-  pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &p->tch[2], &p->vw[2], &p->smem_c_bwd);
-  {
-#ifdef FNO_DEV_KNOBS   // development builds only: FNO_PASS_C_LEGACY=1 keeps the generic pass_c kernels
-    const char* legacy = std::getenv("FNO_PASS_C_LEGACY");
-#else
-    const char* legacy = nullptr;
-#endif
-    if (!(legacy && legacy[0] == '1')) {
-      int cp, tch, vw, nx;
-      size_t sm;
-      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &vw, &sm, &nx)) {
-        p->c2cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->vw[EPI_FWD] = vw; p->smem_c_fwd = sm; p->c2nx[EPI_FWD] = nx;
-      }
-      if (pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_BWD, &cp, &tch, &vw, &sm, &nx)) {
-        p->c2cp[EPI_BWD] = cp; p->tch[EPI_BWD] = tch; p->vw[EPI_BWD] = vw; p->smem_c_bwd = sm; p->c2nx[EPI_BWD] = nx;
-      }
-      if (pass_c3_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, EPI_FWD, &cp, &tch, &sm)) {
-        p->c3cp[EPI_FWD] = cp; p->tch[EPI_FWD] = tch; p->smem_c_fwd = sm;
-      }
-#ifdef FNO_DEV_KNOBS
-      const char* c4e = std::getenv("FNO_PASS_C4");
-      const bool c4_on = !(c4e && c4e[0] == '0');
-#else
-      const bool c4_on = true;
-#endif
-      for (int m = 0; m < 3 && c4_on; ++m) {
-        // layer epilogues: pass_c4 only where no pass_c2 / pass_c3 kernel covers the shape (being tuned)
-        if (m != EPI_U && (p->c2cp[m] > 0 || p->c3cp[m] > 0) && !kC4Layer) continue;
-        int ns;
-        if (pass_c4_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, m, &cp, &ns, &sm)) {
-          p->c4cp[m] = cp; p->c4ns[m] = ns; p->c4smem[m] = sm;
-        }
-      }
+  // pass C kernel families eligible for each epilogue mode
+  for (int m = 0; m < 3; ++m) {
+    fno_plan_s::KCfg& g = p->kc[0][m];
+    g.cp = p->C;
+    pass_c_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, m, &g.tch, &g.vw, &g.smem);
+    int cp, tch, vw, nx, ns;
+    size_t sm;
+    if (m != EPI_U && pass_c2_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, m, &cp, &tch, &vw, &sm, &nx)) {
+      fno_plan_s::KCfg& h = p->kc[1][m];
+      h.cp = cp; h.tch = tch; h.vw = vw; h.smem = sm; h.nx = nx;
+    }
+    if (m == EPI_FWD && pass_c3_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, m, &cp, &tch, &sm)) {
+      fno_plan_s::KCfg& h = p->kc[2][m];
+      h.cp = cp; h.tch = tch; h.smem = sm;
+    }
+    if (pass_c4_config(p->C, int(p->Z), int(p->T), p->mz, p->mt, p->LZ, m, &cp, &ns, &sm)) {
+      fno_plan_s::KCfg& h = p->kc[3][m];
+      h.cp = cp; h.tch = 128 / p->LZ; h.nx = ns; h.smem = sm;
     }
   }
+  // default choice, by measurement on B200 (profiles/r02/ab_pass_c.md): the
+  // spectral u path on pass_c4; the layer forward on pass_c3 where it tiles T
+  // (T % 4 == 0), else pass_c4 (c3: 1.28 vs 1.37 ms); the layer backward on the
+  // FFMA pass_c2 (c2: 0.80 vs 2.05 ms for the tcgen05 pass_c4 backward, whose
+  // three operand splits and single-buffered operands serialise the tile pipeline)
+  auto ok = [&](int f, int m) { return p->kc[f - 1][m].cp > 0; };
+  p->fam[EPI_U] = ok(4, EPI_U) ? 4 : 1;
+  p->fam[EPI_FWD] = (ok(3, EPI_FWD) && p->T % 4 == 0) ? 3 : ok(4, EPI_FWD) ? 4 : ok(3, EPI_FWD) ? 3 : ok(2, EPI_FWD) ? 2 : 1;
+  p->fam[EPI_BWD] = ok(2, EPI_BWD) ? 2 : ok(4, EPI_BWD) ? 4 : 1;
+#ifdef FNO_DEV_KNOBS   // development builds only: FNO_PASS_C_FAM=<u><fwd><bwd> digits force families
+  if (const char* fe = std::getenv("FNO_PASS_C_FAM")) {
+    for (int m = 0; m < 3 && fe[m]; ++m) {
+      const int f = fe[m] - '0';
+      if (f >= 1 && f <= 4 && ok(f, m)) p->fam[m] = f;
+    }
+  }
+#endif
   const size_t smem_max = 227 * 1024;
-  if (p->smem_a[MODE_DZ_GELU] > smem_max || p->smem_c_bwd > smem_max) {
+  if (p->smem_a[MODE_DZ_GELU] > smem_max || p->kc[0][EPI_BWD].smem > smem_max) {
     char buf[200];
     std::snprintf(buf, sizeof buf, "fno_plan_create: shared memory per CTA too large (pass A %zu, pass C %zu bytes)",
-                  p->smem_a[MODE_DZ_GELU], p->smem_c_bwd);
+                  p->smem_a[MODE_DZ_GELU], p->kc[0][EPI_BWD].smem);
     delete p;
     return fail(FNO_ERR_PLAN, buf);
   }
@@ -382,11 +380,14 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
     const int per_sm = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (smem + 1024))));
     return int(std::max<long long>(1, std::min<long long>(n_cols, (long long)p->num_sms * per_sm)));
   };
-  p->grid_c = grid_for(p->smem_c_fwd);
-  p->grid_c_bwd = grid_for(p->smem_c_bwd);
-  p->grid_c_u = grid_for(p->smem_c_u);
-  p->c4grid = int(std::max<long long>(1, std::min<long long>(n_cols, p->num_sms)));
-  p->max_grid_c = std::max(p->grid_c_bwd, p->c4grid);
+  p->max_grid_c = 1;
+  for (int f = 0; f < 4; ++f)
+    for (int m = 0; m < 3; ++m) {
+      fno_plan_s::KCfg& g = p->kc[f][m];
+      g.grid = f == 3 ? int(std::max<long long>(1, std::min<long long>(n_cols, p->num_sms)))   // one CTA per SM
+                      : grid_for(g.smem);
+      if (g.cp > 0) p->max_grid_c = std::max(p->max_grid_c, g.grid);
+    }
 
   // workspace layout
   p->mloc = 4LL * p->mx * p->my * p->nkz * p->mt;
@@ -531,10 +532,19 @@ extern "C" fno_status fno_plan_peer_enabled(fno_plan_t p, int* enabled) {
 extern "C" fno_status fno_plan_pass_c_info(fno_plan_t p, int mode, int64_t info[4]) {
   if (!p || !info || mode < 0 || mode > 2) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_pass_c_info: bad arguments");
   const int m = mode == 0 ? EPI_U : (mode == 1 ? EPI_FWD : EPI_BWD);
-  if (p->c4cp[m] > 0) { info[0] = 4; info[1] = p->c4cp[m]; info[2] = p->c4ns[m]; info[3] = int64_t(p->c4smem[m]); }
-  else if (p->c3cp[m] > 0) { info[0] = 3; info[1] = p->c3cp[m]; info[2] = 0; info[3] = int64_t(p->smem_c_fwd); }
-  else if (p->c2cp[m] > 0) { info[0] = 2; info[1] = p->c2cp[m]; info[2] = p->c2nx[m]; info[3] = int64_t(m == EPI_FWD ? p->smem_c_fwd : p->smem_c_bwd); }
-  else { info[0] = 1; info[1] = p->C; info[2] = 0; info[3] = int64_t(m == EPI_U ? p->smem_c_u : (m == EPI_FWD ? p->smem_c_fwd : p->smem_c_bwd)); }
+  const int f = p->fam[m];
+  const auto& g = p->kc[f - 1][m];
+  info[0] = f; info[1] = g.cp; info[2] = g.nx; info[3] = int64_t(g.smem);
+  return FNO_OK;
+}
+
+extern "C" fno_status fno_plan_set_pass_c(fno_plan_t p, int mode, int family) {
+  if (!p || mode < 0 || mode > 2 || family < 1 || family > 4)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_pass_c: mode 0..2, family 1..4");
+  const int m = mode == 0 ? EPI_U : (mode == 1 ? EPI_FWD : EPI_BWD);
+  if (p->kc[family - 1][m].cp == 0)
+    return fail(FNO_ERR_PLAN, "fno_plan_set_pass_c: that pass C kernel family does not cover this problem");
+  p->fam[m] = family;
   return FNO_OK;
 }
 
@@ -728,9 +738,6 @@ MixParams make_mix(fno_plan_t p) {
 
 PassCParams make_c(fno_plan_t p, int mode) {
   PassCParams c{};
-  c.TCH = p->tch[mode];
-  c.VW = p->vw[mode];
-  c.NX = p->c2nx[mode];
 #ifdef FNO_ABLATE_BUILD
   {
     static const int ablate = [] { const char* e = std::getenv("FNO_ABLATE"); return e ? std::atoi(e) : 0; }();
@@ -738,6 +745,7 @@ PassCParams make_c(fno_plan_t p, int mode) {
   }
 #endif
   c.in = wsp<float2>(p, p->o_slab_xy);
+  c.dWpart = wsp<float>(p, p->o_dwpart);   // bwd: dW / db partial rows (profiling builds: role timers)
   c.n_cols = (long long)p->B * p->Xl * p->Yl;
   c.B = p->B; c.C = p->C; c.Xl = int(p->Xl); c.Yl = int(p->Yl); c.Z = int(p->Z); c.T = int(p->T);
   c.mz = p->mz; c.mt = p->mt; c.Qz = p->Qz; c.Qt = p->Qt;
@@ -747,25 +755,31 @@ PassCParams make_c(fno_plan_t p, int mode) {
   return c;
 }
 
-// the preferred pass C kernel for the mode; *grid_used: its CTA count (the
-// number of dW / db partial rows of the backward)
-cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c0, int mode, int grid, size_t smem, cudaStream_t st,
-                       int* grid_used = nullptr) {
-  if (p->c4cp[mode] > 0) {
+// the selected pass C kernel for the mode (p->fam); *grid_used: its CTA count
+// (the number of dW / db partial rows of the backward).  pass_c4 falls back to
+// the next eligible family when the tensors' alignment rules out its TMA view.
+cudaError_t run_pass_c(fno_plan_t p, const PassCParams& c0, int mode, cudaStream_t st, int* grid_used = nullptr) {
+  int f = p->fam[mode];
+  for (;;) {
+    const auto& g = p->kc[f - 1][mode];
     PassCParams c = c0;
-    c.NX = p->c4ns[mode];
-    cudaError_t e = launch_pass_c4(c, p->LZ, p->LT, p->c4cp[mode], mode, p->c4grid, p->c4smem[mode], st);
-    if (e != cudaErrorNotSupported) {
-      if (grid_used) *grid_used = p->c4grid;
-      return e;
+    c.TCH = g.tch;
+    c.VW = g.vw;
+    c.NX = g.nx;
+    if (grid_used) *grid_used = g.grid;
+    switch (f) {
+      case 4: {
+        const cudaError_t e = launch_pass_c4(c, p->LZ, p->LT, g.cp, mode, g.grid, g.smem, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+        f = p->kc[2][mode].cp ? 3 : p->kc[1][mode].cp ? 2 : 1;
+        continue;
+      }
+      case 3: return launch_pass_c3(c, p->LZ, p->LT, g.cp, g.grid, g.smem, st);
+      case 2: return launch_pass_c2(c, p->LZ, p->LT, g.cp, mode, g.grid, g.smem, st);
+      default: return launch_pass_c(c, p->LZ, p->LT, mode, g.grid, g.smem, st);
     }
-    cudaGetLastError();   // alignment rules out the TMA view: older kernels below
   }
-  if (grid_used) *grid_used = grid;
-  const PassCParams& c = c0;
-  if (p->c3cp[mode] > 0) return launch_pass_c3(c, p->LZ, p->LT, p->c3cp[mode], grid, smem, st);
-  if (p->c2cp[mode] > 0) return launch_pass_c2(c, p->LZ, p->LT, p->c2cp[mode], mode, grid, smem, st);
-  return launch_pass_c(c, p->LZ, p->LT, mode, grid, smem, st);
 }
 
 fno_status check_ready(fno_plan_t p, const char* who) {
@@ -826,7 +840,7 @@ fno_status sb_stage_b(fno_plan_t p, const float2* R, const float2* vhat_saved, f
 fno_status stage_c_u(fno_plan_t p, float* out, cudaStream_t st) {
   PassCParams c = make_c(p, EPI_U);
   c.out = out;
-  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_U, p->grid_c_u, p->smem_c_u, st), "pass C (u)");
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_U, st), "pass C (u)");
   return FNO_OK;
 }
 
@@ -835,7 +849,7 @@ fno_status stage_c_fwd(fno_plan_t p, const float* v, const float* W, const float
                        cudaStream_t st) {
   PassCParams c = make_c(p, EPI_FWD);
   c.v = v; c.W = W; c.bias = b; c.out = y; c.zsave = z_save;
-  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_FWD, p->grid_c, p->smem_c_fwd, st), "pass C (layer forward)");
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_FWD, st), "pass C (layer forward)");
   return FNO_OK;
 }
 
@@ -847,8 +861,8 @@ fno_status stage_c_bwd(fno_plan_t p, const float* v, const float* dz, const floa
   PassCParams c = make_c(p, EPI_BWD);
   c.v = v; c.dy = dz; c.W = W; c.out = dv;
   c.dWpart = wsp<float>(p, p->o_dwpart);
-  int nparts = p->grid_c_bwd;
-  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, p->grid_c_bwd, p->smem_c_bwd, st, &nparts), "pass C (layer backward)");
+  int nparts = 1;
+  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, st, &nparts), "pass C (layer backward)");
   const int len = p->C * p->C + p->C;
   if (!loc) {
     FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, nparts, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");

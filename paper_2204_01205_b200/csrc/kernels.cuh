@@ -12,6 +12,9 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef FNO_MBAR_DEBUG
+#include <cstdio>
+#endif
 
 #include "fft.cuh"
 
@@ -165,11 +168,39 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  if (mbar_try_wait(bar, phase)) return;
-  const unsigned long long t0 = global_ns();
+  if (mbar_test(bar, phase)) return;
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+#ifdef FNO_MBAR_SUSPEND
   while (!mbar_try_wait(bar, phase)) {
-    if (global_ns() - t0 > 4000000000ull) __trap();
+#else
+  // plain polling: the suspend-hint form (NANOSLEEP.SYNCS) was measured to
+  // add wake-up latency to every producer -> consumer hand-off
+  while (!mbar_test(bar, phase)) {
+#endif
+    if ((++n & 1023u) == 0) {   // the deadline is checked rarely: the timer read is not free
+      const unsigned long long t = global_ns();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) {
+#ifdef FNO_MBAR_DEBUG   // development builds: report the stuck barrier instead of trapping
+        printf("mbar timeout: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x,
+               smem_u32(bar), phase);
+        return;
+#else
+        __trap();
+#endif
+      }
+    }
   }
 }
 

@@ -9,11 +9,13 @@
 
 namespace fno {
 
-// padded channel width of the pass_c4 instantiations
+// padded channel width of the pass_c4 instantiations: 4, 8 and the paper's
+// width 20 (C = 9..20 pads to 20: padded channels carry zeros); C > 20 keeps
+// the generic pass_c
 static int c4_cp_of(int C) {
-  if (C <= 20) return (C + 3) & ~3;
-  if (C <= 24) return 24;
-  if (C <= 32) return 32;
+  if (C <= 4) return 4;
+  if (C <= 8) return 8;
+  if (C <= 20) return 20;
   return 0;
 }
 
@@ -33,11 +35,15 @@ bool pass_c4_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
     *CPo = CP; *NS = 1; *smem = s;
     return true;
   }
-  for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= 2; --ns) {
-    const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, ns).total;
-    if (s <= cap) {
-      *CPo = CP; *NS = ns; *smem = s;
-      return true;
+  // preference: four U buffers with an input ring of >= 3 stages, then two U
+  // buffers with the deepest ring (>= 2)
+  for (int nub : {4, 2}) {
+    for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= (nub == 4 ? 3 : 2); --ns) {
+      const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, ns, nub).total;
+      if (s <= cap) {
+        *CPo = CP; *NS = ns | (nub << 8); *smem = s;
+        return true;
+      }
     }
   }
   return false;
@@ -69,11 +75,7 @@ cudaError_t launch_pass_c4(const PassCParams& p0, int LZ, int LT, int CP, int mo
   switch (CP) {
     FNO_C4_CP(4)
     FNO_C4_CP(8)
-    FNO_C4_CP(12)
-    FNO_C4_CP(16)
     FNO_C4_CP(20)
-    FNO_C4_CP(24)
-    FNO_C4_CP(32)
     default: return cudaErrorInvalidValue;
   }
 #undef FNO_C4_CP

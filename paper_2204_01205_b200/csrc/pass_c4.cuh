@@ -24,14 +24,18 @@
 //                    v' = v rows and a ones row (-> db); A2 stores only the
 //                    ceil(C/8) real row groups, the M = 128 over-read lands in
 //                    the following K groups (rows >= C of D2 are never read)
-//   warps 0-3    split + epilogue (thread = tile point = TMEM lane): splits
-//                tile k into the K-major tf32 hi / lo operands, then finishes
-//                tile k-1: D1 row + U column (fwd: GELU, z) -> float4 stores;
-//                bwd: warp 0 adds the D2 rows (dW, db) of every tile into fp32
-//                registers (a per-tile flush keeps the tensor-core sums short)
-//   warps 6-11   transforms: per column phase 1 (inverse t of the slab, C2R
-//                weights and 1/N folded in -> Bb), per tile phase 2 (inverse z
+//   warps 0-3,   two split + epilogue warpgroups, even and odd tiles (thread =
+//   8-11         tile point = TMEM lane; warps w and w + 8 share the lane
+//                quarter w): each splits its tile k into the K-major tf32 hi /
+//                lo operands, then finishes its previous tile k-2: D1 row + U
+//                column (fwd: GELU, z) -> float4 stores; bwd: warps 0 and 8 add
+//                the D2 rows (dW, db) of every tile into fp32 registers (a
+//                per-tile flush keeps the tensor-core sums short)
+//   warps 6, 7,  transforms: per column phase 1 (inverse t of the slab, C2R
+//   12-15        weights and 1/N folded in -> Bb), per tile phase 2 (inverse z
 //                of residue class rz -> U[k & 1])
+// 16 warps at <= 128 registers; the two epilogue warpgroups give the
+// latency-bound epilogue (TMEM load, U, GELU, float4 stores) two tiles in flight.
 //
 // fp32 accuracy from tf32 operands (3xTF32): x = hi + lo with hi the tf32
 // truncation of x and lo = x - hi; D = A_hi B_hi + A_lo B_hi + A_hi B_lo.
@@ -51,9 +55,9 @@
 
 namespace fno {
 
-constexpr int C4T = 384;            // 12 warps
-constexpr int C4_NTT = 192;         // transform threads (warps 6-11)
-constexpr int C4_PROD = 4, C4_MMA = 5, C4_TR0 = 6;
+constexpr int C4T = 512;            // 16 warps
+constexpr int C4_NTT = 192;         // transform threads (warps 6, 7, 12-15)
+constexpr int C4_PROD = 4, C4_MMA = 5;
 constexpr int C4_MAXNS = 6;
 
 __host__ __device__ constexpr int c4_kp(int CP, int mode) {
@@ -67,14 +71,18 @@ __host__ __device__ constexpr int c4_tmem_cols(int CP, int mode) {
 }
 
 struct C4Layout {
-  int NS, NOB, KP, NP, NW, RG, nk, TP, UPS;
-  size_t x, xstage, op, opstage, a1hi, a1lo, a2hi, a2lo, b2hi, b2lo, b1hi, b1lo, bb, u0, u1, twz, twt, dmap, bar, slot,
-      total;
+  int NS, NUB, NOB, KP, NP, NW, RG, nk, TP, UPS;
+  size_t x, xstage, op, opstage, a1hi, a1lo, a2hi, a2lo, b2hi, b2lo, b1hi, b1lo, bb, u0, ustride, twz, twt, dmap, bar, slot,
+      red, total;
 };
 
-// NS: input-tile ring stages; operand buffers: 2 (fwd), 1 (bwd)
-__host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, int T, int mz, int LZ, int NS) {
+// NS: input-tile ring stages; NUB: U buffers (2, or 4 = two per epilogue
+// warpgroup, so the transforms run a tile further ahead); operand buffers: 2
+// (fwd), 1 (bwd)
+__host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, int T, int mz, int LZ, int NS,
+                                              int NUB = 2) {
   C4Layout L{};
+  L.NUB = NUB;
   const bool bwd = mode == EPI_BWD, mma = mode != EPI_U;
   L.NS = mma ? NS : 0;
   L.NOB = mode == EPI_FWD ? 2 : (bwd ? 1 : 0);
@@ -107,17 +115,36 @@ __host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, in
   L.b1hi = take(size_t(L.NP) * L.KP * sizeof(float));
   L.b1lo = take(size_t(L.NP) * L.KP * sizeof(float));
   L.bb = take(size_t(C) * L.nk * L.TP * sizeof(float2));
-  L.u0 = take(size_t(C) * L.UPS * sizeof(float));
-  L.u1 = take(size_t(C) * L.UPS * sizeof(float));
+  L.ustride = (size_t(C) * L.UPS * sizeof(float) + 1023) & ~size_t(1023);
+  L.u0 = take(L.ustride * NUB);
   auto take16 = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
   L.twz = take16(size_t(Z) * sizeof(float2));
   L.twt = take16(size_t(T) * sizeof(float2));
   L.dmap = take16(size_t(2 * mz) * sizeof(short2));
   L.bar = take16(32 * sizeof(uint64_t));
   L.slot = take16(sizeof(uint32_t));
-  L.total = off + 1024;   // + alignment slack of the dynamic shared memory base
+  L.red = take16(bwd ? size_t(2) * 32 * L.NW * sizeof(float) : 16);   // dW / db sums of the two warpgroups
+  L.total = off;
   return L;
 }
+
+// Development builds (-DFNO_C4_PROFILE, scripts/variant_libs.sh): per-CTA
+// clock64 timers of each role's waits and work, written over the (forward-
+// unused) dW partial rows: slot i of CTA b at ((u64*)p.dWpart)[16 b + i].
+#ifdef FNO_C4_PROFILE
+#define C4P_DECL unsigned long long c4p[16] = {0};
+#define C4P_T(v) const long long v = clock64();
+#define C4P_ADD(slot, v) c4p[slot] += (unsigned long long)(clock64() - (v));
+#define C4P_DUMP(cond, first, n)                                                               \
+  if ((cond) && EPI != EPI_BWD)                                                                \
+    for (int i_ = 0; i_ < (n); ++i_)                                                           \
+      reinterpret_cast<unsigned long long*>(p.dWpart)[16ll * blockIdx.x + (first) + i_] = c4p[(first) + i_];
+#else
+#define C4P_DECL
+#define C4P_T(v)
+#define C4P_ADD(slot, v)
+#define C4P_DUMP(cond, first, n)
+#endif
 
 // K-major (SWIZZLE_NONE) element offset, RGS row groups of 8 rows per K group of 4
 __device__ __forceinline__ int kmaj_rows(int row, int k, int RGS) {
@@ -136,25 +163,27 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
   constexpr int NCH1 = (CP + 7) / 8;
   constexpr int NOB = EPI == EPI_FWD ? 2 : 1;
   constexpr uint32_t TMEM_COLS = c4_tmem_cols(CP, EPI);
-  extern __shared__ __align__(1024) unsigned char smem_dyn[];
-  unsigned char* smem_raw =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  // (no run-time realignment of the base: pointer arithmetic through an
+  // integer cast loses the shared state space and turns every operand access
+  // into a generic LD / ST; SWIZZLE_NONE operands and TMA boxes need 128 B)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
-  const int NS = MMA ? p.NX : 1;
-  const C4Layout L = c4_layout(CP, EPI, C, Z, T, mz, LZ, NS);
+  const int NS = MMA ? (p.NX & 255) : 1;
+  const int NUB = (p.NX >> 8) == 4 ? 4 : 2;
+  const C4Layout L = c4_layout(CP, EPI, C, Z, T, mz, LZ, NS, NUB);
   float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
   float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
   float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
   short2* dmap = reinterpret_cast<short2*>(smem_raw + L.dmap);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
   uint64_t* xfull = bars;          // [NS]  TMA bytes landed
-  uint64_t* xempty = bars + 8;     // [NS]  128 split threads done reading
-  uint64_t* opfull = bars + 16;    // [2]   128 split threads wrote the operands
+  uint64_t* xempty = bars + 8;     // [NS]  4 split warps done reading
+  uint64_t* opfull = bars + 16;    // [2]   4 split warps wrote the operands
   uint64_t* opempty = bars + 18;   // [2]   MMAs done reading them (tcgen05.commit)
   uint64_t* dfull = bars + 20;     // [2]   MMAs done writing D[b] (tcgen05.commit)
-  uint64_t* dempty = bars + 22;    // [2]   128 epilogue threads read D[b]
-  uint64_t* ufull = bars + 24;     // [2]   192 transform threads wrote U[b]
-  uint64_t* uempty = bars + 26;    // [2]   128 epilogue threads read U[b]
+  uint64_t* dempty = bars + 22;    // [2]   4 epilogue warps read D[b]
+  uint64_t* ufull = bars + 24;     // [NUB] 6 transform warps wrote U[k % NUB]
+  uint64_t* uempty = bars + 28;    // [NUB] 4 epilogue warps read U[k % NUB]
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem_raw + L.slot);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk = L.nk, TP = L.TP, UPS = L.UPS;
@@ -220,17 +249,22 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
     }
   }
   if (tid == 0) {
+    // consumer / producer groups arrive once per warp (lane 0 after a
+    // __syncwarp): every mbarrier event wakes the warps sleeping in try_wait,
+    // so per-thread arrivals would keep the waiting roles spinning
     for (int s = 0; s < NS && MMA; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], 128);
+      mbar_init(&xempty[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&opfull[b], 128);
+      mbar_init(&opfull[b], 4);
       mbar_init(&opempty[b], 1);
       mbar_init(&dfull[b], 1);
-      mbar_init(&dempty[b], 128);
-      mbar_init(&ufull[b], C4_NTT);
-      mbar_init(&uempty[b], 128);
+      mbar_init(&dempty[b], 4);
+    }
+    for (int b = 0; b < NUB; ++b) {
+      mbar_init(&ufull[b], C4_NTT / 32);
+      mbar_init(&uempty[b], 4);
     }
     mbar_fence_init();
   }
@@ -247,9 +281,12 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
     return int(cu - unsigned(*b_out) * per_b);
   };
   // first t of tile ti (TMA row groups with (z T) % 4 != 0 start early, c2_tile_group)
-  auto tile_t0 = [&](int ti) {
-    const int rz = ti / nch, tc = ti - rz * nch;
+  auto tile_t0 = [&](int rz, int tc) {
     return tc * TCH - ((RAG && p.tma_g > 1) ? ((rz & (p.tma_g - 1)) * T) & 3 : 0);
+  };
+  // (rz, tc) of the next tile: t chunks innermost (ti = rz * nch + tc)
+  auto next_tile = [&](int& rz, int& tc) {
+    if (++tc == nch) { tc = 0; ++rz; }
   };
   auto xstage = [&](int s) { return reinterpret_cast<float*>(smem_raw + L.x + s * L.xstage); };
   auto opbuf = [&](int ob) { return smem_raw + L.op + ob * L.opstage; };
@@ -257,23 +294,27 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
   if (warp == C4_PROD) {
     // ======================= TMA producer ========================================
     if (MMA && lane == 0) {
-      unsigned k = 0;
+      C4P_DECL
+      int s = 0;
+      unsigned xph = 0;   // parity of the ring's current pass
       for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
         int bb;
         const int xy = col_split(col, &bb);
-        for (int ti = 0; ti < tpc; ++ti, ++k) {
-          const int s = int(k % unsigned(NS));
-          const unsigned u = k / unsigned(NS);
-          mbar_wait(&xempty[s], (u & 1u) ^ 1u);
+        int rz = 0, tc = 0;
+        for (int ti = 0; ti < tpc; ++ti, next_tile(rz, tc)) {
+          C4P_T(tw0)
+          mbar_wait(&xempty[s], xph ^ 1u);
+          C4P_ADD(0, tw0)
           mbar_expect_tx(&xfull[s], tile_bytes * NA);
-          const int rz = ti / nch, tc = ti - rz * nch;
-          const int r = (rz % p.tma_g) * T;
+          const int r = (rz & (p.tma_g - 1)) * T;
 #pragma unroll
           for (int a = 0; a < NA; ++a)
             tma_load_5d(xstage(s) + a * C * 128, &maps.m[a], r + tc * TCH - (r & 3), rz / p.tma_g, 0, xy, bb * C,
                         &xfull[s]);
+          if (++s == NS) { s = 0; xph ^= 1u; }
         }
       }
+      C4P_DUMP(true, 0, 1)
     }
   } else if (warp == C4_MMA) {
     // ======================= MMA issuer ==========================================
@@ -282,66 +323,72 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
       const uint32_t idesc2 = umma_idesc_tf32(128, NW, 0, 0);
       constexpr uint32_t A1_LBO = (128 / 8) * 128, B1_LBO = (NP / 8) * 128;
       constexpr uint32_t A2_LBO = RG * 128, B2_LBO = (NW / 8) * 128;
-      const float* B1hi = reinterpret_cast<const float*>(smem_raw + L.b1hi);
-      const float* B1lo = reinterpret_cast<const float*>(smem_raw + L.b1lo);
+      // descriptors of operand buffer 0 and K step 0; the start address field
+      // (bits 0-13, 16-byte units) advances by plain 64-bit adds
+      const uint64_t a1hi0 = umma_sdesc(opbuf(0) + L.a1hi, A1_LBO, 128);
+      const uint64_t a1lo0 = umma_sdesc(opbuf(0) + L.a1lo, A1_LBO, 128);
+      const uint64_t b1hi0 = umma_sdesc(smem_raw + L.b1hi, B1_LBO, 128);
+      const uint64_t b1lo0 = umma_sdesc(smem_raw + L.b1lo, B1_LBO, 128);
+      const uint64_t a2hi0 = umma_sdesc(opbuf(0) + L.a2hi, A2_LBO, 128);
+      const uint64_t a2lo0 = umma_sdesc(opbuf(0) + L.a2lo, A2_LBO, 128);
+      const uint64_t b2hi0 = umma_sdesc(opbuf(0) + L.b2hi, B2_LBO, 128);
+      const uint64_t b2lo0 = umma_sdesc(opbuf(0) + L.b2lo, B2_LBO, 128);
+      const uint64_t obstep = uint64_t(L.opstage >> 4);
+      C4P_DECL
       unsigned k = 0;
       for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
         for (int ti = 0; ti < tpc; ++ti, ++k) {
           const int b = k & 1;
           const unsigned u = k >> 1;
           const int ob = NOB == 2 ? b : 0;
-          const unsigned ou = NOB == 2 ? u : k;
-          mbar_wait(&opfull[ob], ou & 1u);
+          C4P_T(tm0)
+          mbar_wait(&opfull[b], u & 1u);   // tile k's operands (per-parity barrier: no phase aliasing)
+          C4P_ADD(1, tm0)
+          C4P_T(tm1)
           mbar_wait(&dempty[b], (u & 1u) ^ 1u);
+          C4P_ADD(2, tm1)
           tc_fence_after();
-          const unsigned char* base = opbuf(ob);
-          const float* A1hi = reinterpret_cast<const float*>(base + L.a1hi);
-          const float* A1lo = reinterpret_cast<const float*>(base + L.a1lo);
+          const uint64_t oo = uint64_t(ob) * obstep;
           const uint32_t d1 = tmem + 32u * b;
 #pragma unroll
           for (int j = 0; j < KP / 8; ++j) {
-            const uint64_t ah = umma_sdesc(A1hi + j * 2 * (A1_LBO / 4), A1_LBO, 128);
-            const uint64_t al = umma_sdesc(A1lo + j * 2 * (A1_LBO / 4), A1_LBO, 128);
-            const uint64_t bh = umma_sdesc(B1hi + j * 2 * (B1_LBO / 4), B1_LBO, 128);
-            const uint64_t bl = umma_sdesc(B1lo + j * 2 * (B1_LBO / 4), B1_LBO, 128);
-            umma_tf32(d1, ah, bh, idesc1, j > 0 ? 1u : 0u);
-            umma_tf32(d1, al, bh, idesc1, 1u);
-            umma_tf32(d1, ah, bl, idesc1, 1u);
+            const uint64_t ja = uint64_t(j) * ((2 * A1_LBO) >> 4), jb = uint64_t(j) * ((2 * B1_LBO) >> 4);
+            umma_tf32(d1, a1hi0 + oo + ja, b1hi0 + jb, idesc1, j > 0 ? 1u : 0u);
+            umma_tf32(d1, a1lo0 + oo + ja, b1hi0 + jb, idesc1, 1u);
+            umma_tf32(d1, a1hi0 + oo + ja, b1lo0 + jb, idesc1, 1u);
           }
           if (BWD) {
-            const float* A2hi = reinterpret_cast<const float*>(base + L.a2hi);
-            const float* A2lo = reinterpret_cast<const float*>(base + L.a2lo);
-            const float* B2hi = reinterpret_cast<const float*>(base + L.b2hi);
-            const float* B2lo = reinterpret_cast<const float*>(base + L.b2lo);
             const uint32_t d2 = tmem + 64u + uint32_t(NW) * b;
-#pragma unroll 4
-            for (int j = 0; j < 128 / 8; ++j) {
-              const uint64_t ah = umma_sdesc(A2hi + j * 2 * (A2_LBO / 4), A2_LBO, 128);
-              const uint64_t al = umma_sdesc(A2lo + j * 2 * (A2_LBO / 4), A2_LBO, 128);
-              const uint64_t bh = umma_sdesc(B2hi + j * 2 * (B2_LBO / 4), B2_LBO, 128);
-              const uint64_t bl = umma_sdesc(B2lo + j * 2 * (B2_LBO / 4), B2_LBO, 128);
+            uint64_t ah = a2hi0 + oo, al = a2lo0 + oo, bh = b2hi0 + oo, bl = b2lo0 + oo;
+#pragma unroll 2
+            for (int j = 0; j < 128 / 8; ++j) {   // loop-carried descriptors (few registers)
               umma_tf32(d2, ah, bh, idesc2, j > 0 ? 1u : 0u);
               umma_tf32(d2, al, bh, idesc2, 1u);
               umma_tf32(d2, ah, bl, idesc2, 1u);
+              ah += (2 * A2_LBO) >> 4; al += (2 * A2_LBO) >> 4;
+              bh += (2 * B2_LBO) >> 4; bl += (2 * B2_LBO) >> 4;
             }
           }
-          umma_commit(&opempty[ob]);
+          umma_commit(&opempty[b]);
           umma_commit(&dfull[b]);
         }
       }
+      C4P_DUMP(true, 1, 2)
     }
-  } else if (warp >= C4_TR0) {
+  } else if (warp == 6 || warp == 7 || warp >= 12) {
     // ======================= transforms (phases 1-2) ===============================
-    const int ttid = tid - C4_TR0 * 32;
+    const int ttid = (warp < 8 ? warp - 6 : warp - 10) * 32 + lane;
     auto slab_at = [&](long long c_, int c, int jz) -> const float2* {
       if (p.slab.P == 1) return p.in + (c_ * C + c) * per_c + jz * mt;
       const short2 dm = dmap[jz];
       const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
       return p.in + p.slab.off[dm.x] + ((c_ * C + c) * nkz + dm.y) * mt;
     };
+    C4P_DECL
     unsigned k = 0;
     for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
       const long long col_next = col + gridDim.x;
+      C4P_T(tp1)
       group_sync(2, C4_NTT);   // the previous column's phase 2 is done with Bb
       // ---- phase 1: inverse t (C2R weights and 1/N folded in), items (c, kz', rt)
       for (int it = ttid; it < C * nk * p.Qt; it += C4_NTT) {
@@ -372,16 +419,24 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
         for (int s = 0; s < LT; ++s) bo[p.Qt * s] = cscale(y[s], p.inv_n);   // the 1/N of the inverse
       }
       group_sync(2, C4_NTT);   // Bb complete
+      C4P_ADD(8, tp1)
       if (col_next < p.n_cols)   // next column's slab rows into L1 (phase 1 then hits L1)
         for (int r = ttid; r < C * 2 * mz; r += C4_NTT)
           asm volatile("prefetch.global.L1 [%0];" ::"l"(slab_at(col_next, r / (2 * mz), r % (2 * mz))));
-      for (int ti = 0; ti < tpc; ++ti, ++k) {
-        const int rz = ti / nch;
-        const int t0 = tile_t0(ti);
-        const int b = k & 1;
-        const unsigned u = k >> 1;
+      int rz = 0, tc = 0;
+      for (int ti = 0; ti < tpc; ++ti, ++k, next_tile(rz, tc)) {
+        const int t0 = tile_t0(rz, tc);
+        const int b = NUB == 4 ? int(k & 3u) : int(k & 1u);
+        const unsigned u = NUB == 4 ? (k >> 2) : (k >> 1);
+        C4P_T(tp2)
+        // one waiter, the other transform warps park on the named barrier (no
+        // issue slots spent polling)
+        if (ttid == 0) mbar_wait(&uempty[b], (u & 1u) ^ 1u);
+        group_sync(2, C4_NTT);
         mbar_wait(&uempty[b], (u & 1u) ^ 1u);
-        float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
+        C4P_ADD(9, tp2)
+        C4P_T(tp3)
+        float* U = reinterpret_cast<float*>(smem_raw + L.u0 + b * L.ustride);
         // ---- phase 2: inverse z (real output), items (c, tt) -> U[b] -----------
         const int ta = RAG ? max(0, -t0) : 0, tb = RAG ? min(TCH, T - t0) : TCH;
         for (int it = ttid; it < C * TCH; it += C4_NTT) {
@@ -397,35 +452,60 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
 #pragma unroll
           for (int s = 0; s < LZ; ++s) uo[s * TCH] = y[s].x;
         }
-        mbar_arrive(&ufull[b]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ufull[b]);
+        C4P_ADD(10, tp3)
       }
     }
-  } else if (warp < 4) {
-    // ======================= split + epilogue (TMEM lanes) =========================
-    const int et = tid;   // tile point of the epilogue, operand row of the split
-    const uint32_t t_row = tmem + ((uint32_t)(32 * warp) << 16);
-    float dwacc[BWD ? NW : 1];
-#pragma unroll
-    for (int i = 0; i < (BWD ? NW : 1); ++i) dwacc[i] = 0.f;
+    C4P_DUMP(ttid == 0, 8, 3)
+  } else {
+    // ======================= split + epilogue (TMEM lanes), warps 0-3 | 8-11 ========
+    const int ew = warp & 3, wg = warp >> 3;   // lane quarter, warpgroup (even / odd tiles)
+    const int et = ew * 32 + lane;             // tile point of the epilogue, operand row of the split
+    const int gbar = 1 + 2 * wg;               // this warpgroup's named barrier
+    C4P_DECL
+    const uint32_t t_row = tmem + ((uint32_t)(32 * ew) << 16);
+    // bwd: this warpgroup's dW / db running sums (rows o = lane of warp ew == 0)
+    float* dwsum = reinterpret_cast<float*>(smem_raw + L.red) + wg * 32 * NW;
+    if (BWD && ew == 0)
+      for (int i = 0; i < NW; ++i) dwsum[lane * NW + i] = 0.f;
 
     // operands of tile k (col, ti) from its X stage
-    auto split = [&](unsigned k, int ti) {
-      const int s = int(k % unsigned(NS));
-      const unsigned u = k / unsigned(NS);
+    int xs = wg;
+    unsigned xph = 0;   // X ring position of this warpgroup's next split (tiles wg, wg + 2, ...)
+    auto split = [&](unsigned k, int rz, int tc) {
+      const int s = xs;
       const int ob = NOB == 2 ? int(k & 1) : 0;
-      const unsigned ou = NOB == 2 ? (k >> 1) : k;
-      mbar_wait(&xfull[s], u & 1u);
-      mbar_wait(&opempty[ob], (ou & 1u) ^ 1u);
+
+      C4P_T(ts0)
+      if (et == 0) {   // one waiter; the other split threads park on the named barrier
+        mbar_wait(&xfull[s], xph);
+        // operand buffer free: fwd (two buffers) after MMA(k-2), bwd (one buffer,
+        // shared by the two warpgroups) after MMA(k-1) -- each waited on the
+        // per-parity barrier it committed to, so no waiter can be two phases behind
+        if (NOB == 2) mbar_wait(&opempty[k & 1], ((k >> 1) & 1u) ^ 1u);
+        else if (k > 0) mbar_wait(&opempty[(k - 1) & 1], ((k - 1) >> 1) & 1u);
+      }
+      group_sync(gbar, 128);
+      mbar_wait(&xfull[s], xph);   // completed: one test, the acquire of the TMA bytes for this thread
+      xs += 2;
+      if (xs >= NS) { xs -= NS; xph ^= 1u; }
+      C4P_ADD(3, ts0)
+      C4P_T(ts1)
       const float* X0 = xstage(s);   // v (fwd) or dz (bwd): [C][128]
       unsigned char* base = opbuf(ob);
       float* A1hi = reinterpret_cast<float*>(base + L.a1hi);
       float* A1lo = reinterpret_cast<float*>(base + L.a1lo);
       // A1[p][k] = X0[k][p] (K-major, 4 channels per float4)
-      for (int e = et; e < (CP / 4) * 128; e += 128) {
-        const int g = e >> 7, pp = e & 127;
-        float x[4];
+      // (fully unrolled, loads first: the warps of this role are few, so every
+      // hand-off must expose instruction-level parallelism)
+      float xa[CP];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = (4 * g + j < C) ? X0[(4 * g + j) * 128 + pp] : 0.f;
+      for (int k = 0; k < CP; ++k) xa[k] = (k < C) ? X0[k * 128 + et] : 0.f;
+#pragma unroll
+      for (int g = 0; g < CP / 4; ++g) {
+        const int pp = et;
+        const float x[4] = {xa[4 * g], xa[4 * g + 1], xa[4 * g + 2], xa[4 * g + 3]};
         float4 hi, lo;
         hi.x = tf32_hi(x[0]); lo.x = x[0] - hi.x;
         hi.y = tf32_hi(x[1]); lo.y = x[1] - hi.y;
@@ -439,14 +519,14 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
         // of X0; B2[i][p] = v.  Diagonal lane order: each 8-lane phase reads 8
         // distinct chunk columns q and writes 8 distinct rows (bank-conflict free).
         // Points outside [0, T) of a ragged tile are zeroed in A2 (exact dW, db).
-        const int t0 = tile_t0(ti);
+        const int t0 = tile_t0(rz, tc);
         const int ta = RAG ? max(0, -t0) : 0, tb = RAG ? min(TCH, T - t0) : TCH;
         const float* V0 = X0 + C * 128;
         float* A2hi = reinterpret_cast<float*>(base + L.a2hi);
         float* A2lo = reinterpret_cast<float*>(base + L.a2lo);
         float* B2hi = reinterpret_cast<float*>(base + L.b2hi);
         float* B2lo = reinterpret_cast<float*>(base + L.b2lo);
-        const int w = warp, j8 = lane & 7, ph = lane >> 3;
+        const int w = ew, j8 = lane & 7, ph = lane >> 3;
         // blocks of 8 rows x 8 chunk columns: RG x 4 per operand, 2 operands
         for (int blk = w; blk < 2 * RG * 4; blk += 4) {
           const int opnd = blk / (RG * 4), r = blk - opnd * (RG * 4);
@@ -483,60 +563,82 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
           }
         }
       }
-      mbar_arrive(&xempty[s]);   // this thread's reads of the X stage are done
       fence_proxy_async();       // generic-proxy operand stores -> visible to the tensor core
-      mbar_arrive(&opfull[ob]);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&xempty[s]);   // the warp's reads of the X stage are done
+        mbar_arrive(&opfull[k & 1]);
+      }
+      C4P_ADD(4, ts1)
     };
 
     // results of tile k (col, ti): D1 row + U column -> stores; bwd: D2 -> dW, db
-    auto epilogue = [&](unsigned k, long long col, int ti) {
-      const int b = k & 1;
+    auto epilogue = [&](unsigned k, long long col, int rz, int tc) {
+      const int b = k & 1;                      // TMEM D buffer = this warpgroup's
       const unsigned u = k >> 1;
-      float* U = reinterpret_cast<float*>(smem_raw + (b ? L.u1 : L.u0));
-      const int rz = ti / nch;
-      const int t0 = tile_t0(ti);
-      mbar_wait(&ufull[b], u & 1u);
+      const int ub = NUB == 4 ? int(k & 3u) : b;  // U buffer
+      const unsigned uu = NUB == 4 ? (k >> 2) : u;
+      float* U = reinterpret_cast<float*>(smem_raw + L.u0 + ub * L.ustride);
+      const int t0 = tile_t0(rz, tc);
+      C4P_T(te0)
+      if (et == 0) {   // one waiter; the other epilogue threads park on the named barrier
+        mbar_wait(&ufull[ub], uu & 1u);
+        if (MMA) mbar_wait(&dfull[b], u & 1u);
+      }
+      group_sync(gbar, 128);
+      mbar_wait(&ufull[ub], uu & 1u);             // completed: one test each (acquire)
+      if (MMA) mbar_wait(&dfull[b], u & 1u);
+      C4P_ADD(5, te0)
+      C4P_T(te2)
       if (MMA) {
-        mbar_wait(&dfull[b], u & 1u);
         tc_fence_after();
         uint32_t d[NCH1][8];
 #pragma unroll
         for (int q = 0; q < NCH1; ++q) tmem_ld8_nowait(t_row + 32u * b + 8 * q, d[q]);
-        uint32_t d2[BWD ? NW / 8 : 1][8];
-        if (BWD && warp == 0) {
+        if (BWD && ew == 0) {   // D2 rows (dW, db) first, 8 columns at a time: few live registers
+#pragma unroll 1
+          for (int q = 0; q < (BWD ? NW / 8 : 0); ++q) {
+            uint32_t d2[8];
+            tmem_ld8_nowait(t_row + 64u + uint32_t(NW) * b + 8 * q, d2);
+            tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < (BWD ? NW / 8 : 0); ++q) tmem_ld8_nowait(t_row + 64u + uint32_t(NW) * b + 8 * q, d2[q]);
+            for (int j = 0; j < 8; ++j) dwsum[lane * NW + 8 * q + j] += __uint_as_float(d2[j]);
+          }
         }
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&dempty[b]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[b]);
+        float uv[CP];
 #pragma unroll
-        for (int o = 0; o < CP; ++o) {
-          if (o >= C) break;
-          U[o * UPS + et] += __uint_as_float(d[o >> 3][o & 7]);
-        }
-        if (BWD && warp == 0) {
+        for (int o = 0; o < CP; ++o) uv[o] = (o < C) ? U[o * UPS + et] : 0.f;
 #pragma unroll
-          for (int q = 0; q < (BWD ? NW / 8 : 0); ++q)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) dwacc[8 * q + j] += __uint_as_float(d2[q][j]);
-        }
+        for (int o = 0; o < CP; ++o)
+          if (o < C) U[o * UPS + et] = uv[o] + __uint_as_float(d[o >> 3][o & 7]);
+
       }
       __syncwarp();
       int bcol;
       const int xycol = col_split(col, &bcol);
       const long long cbase = (long long)bcol * C * chan_stride + (long long)xycol * ZT;
       // float4 f of the warp: channel o, points 32 warp + 4 (lane % 8) + [0, 4)
-      const int pq = 32 * warp + 4 * (lane & 7);
+      const int pq = 32 * ew + 4 * (lane & 7);
       const int sq = pq / TCH, tq = pq - sq * TCH;
       const long long gq = cbase + (long long)(rz + p.Qz * sq) * T + t0 + tq;
       const int k0 = RAG ? max(0, -(t0 + tq)) : 0, k1 = RAG ? min(4, T - t0 - tq) : 4;
       const bool v4 = !RAG || (k0 == 0 && k1 == 4);   // TMA tiles start 16-byte aligned
+      constexpr int NJ = (CP + 3) / 4;
+      float4 rq[NJ];
 #pragma unroll
-      for (int j = 0; j < (CP + 3) / 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         const int o = (lane >> 3) + 4 * j;
-        if (o >= C || k0 >= k1) break;
-        float4 r = *reinterpret_cast<const float4*>(U + o * UPS + pq);
+        rq[j] = (o < C) ? *reinterpret_cast<const float4*>(U + o * UPS + pq) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int o = (lane >> 3) + 4 * j;
+        if (o >= C || k0 >= k1) continue;
+        float4 r = rq[j];
         const long long g = gq + o * chan_stride;
         if (v4) {
           if (EPI == EPI_FWD) {
@@ -562,33 +664,44 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
         }
       }
       __syncwarp();
-      mbar_arrive(&uempty[b]);   // U[b] free
+      if (lane == 0) mbar_arrive(&uempty[ub]);   // U[ub] free
+      C4P_ADD(7, te2)
     };
 
-    unsigned k = 0;
+    C4P_T(tall)
+    unsigned k = 0, pk = 0;
     long long pcol = -1;
-    int pti = 0;
+    int prz = 0, ptc = 0;
     for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
-      for (int ti = 0; ti < tpc; ++ti, ++k) {
-        if (MMA) split(k, ti);
-        if (pcol >= 0) epilogue(k - 1, pcol, pti);
+      int rz = 0, tc = 0;
+      for (int ti = 0; ti < tpc; ++ti, ++k, next_tile(rz, tc)) {
+        if (int(k & 1u) != wg) continue;   // the other warpgroup's tile
+        if (MMA) split(k, rz, tc);
+        if (pcol >= 0) epilogue(pk, pcol, prz, ptc);
         pcol = col;
-        pti = ti;
+        prz = rz;
+        ptc = tc;
+        pk = k;
       }
     }
-    if (pcol >= 0) epilogue(k - 1, pcol, pti);
-    if (BWD && warp == 0) {
-      // this CTA's dW / db partial row (fixed order: per tile, in tile order)
-      float* outp = p.dWpart + (long long)blockIdx.x * (C * C + C);
-      if (lane < C) {
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-          if (i < C) outp[lane * C + i] = dwacc[i];
-          else if (i == C) outp[C * C + lane] = dwacc[i];
+    if (pcol >= 0) epilogue(pk, pcol, prz, ptc);
+    C4P_ADD(11, tall)
+    C4P_DUMP(tid == 0, 3, 5)
+    C4P_DUMP(tid == 0, 11, 1)
+    tc_fence_before();
+    if (BWD) {
+      // the even (warp 0) and odd (warp 8) tiles' dW / db partials, in a fixed order
+      const float* red = reinterpret_cast<const float*>(smem_raw + L.red);
+      if (warp == 0 || warp == 8) group_sync(4, 64);
+      if (warp == 0 && lane < C) {
+        float* outp = p.dWpart + (long long)blockIdx.x * (C * C + C);
+        for (int i = 0; i <= C; ++i) {
+          const float v = red[lane * NW + i] + red[32 * NW + lane * NW + i];
+          if (i < C) outp[lane * C + i] = v;
+          else outp[C * C + lane] = v;
         }
       }
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (MMA && warp == C4_MMA) {
@@ -622,11 +735,7 @@ cudaError_t launch_c4_case(const C2Maps& maps, const PassCParams& p, int grid, s
 #define FNO_C4_DECL3(cp) FNO_C4_DECL(cp, u) FNO_C4_DECL(cp, fwd) FNO_C4_DECL(cp, bwd)
 FNO_C4_DECL3(4)
 FNO_C4_DECL3(8)
-FNO_C4_DECL3(12)
-FNO_C4_DECL3(16)
 FNO_C4_DECL3(20)
-FNO_C4_DECL3(24)
-FNO_C4_DECL3(32)
 #undef FNO_C4_DECL3
 #undef FNO_C4_DECL
 

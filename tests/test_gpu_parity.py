@@ -327,3 +327,49 @@ def test_wide_channels_fwd_bwd(C):
     dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
     for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
         assert rel_l2(G.np64(got), ref) < TOL, name
+
+
+# Every pass C kernel family the plan can select (fno_plan_set_pass_c), forced on
+# the shapes that exercise their tile geometries: forward and backward vs the
+# oracle.  Families: 2 pass_c2 (FFMA), 3 pass_c3 (tcgen05 1x1), 4 pass_c4
+# (warp-specialised, TMA ring, tcgen05 1x1 / W^T dz / dW).
+FAMILY_CASES = [
+    ((32, 16, 64, 32), 20, (8, 8, 8, 8)),       # c2 class: T % 4 == 0, HALF (2mz = LZ)
+    ((32, 32, 64, 30), 20, (12, 12, 12, 12)),   # c3 class: T = 30, row-group TMA view, ragged chunks
+    ((16, 32, 32, 15), 8, (6, 6, 8, 6)),        # odd T: 4-row groups
+]
+
+
+@pytest.mark.parametrize("family", [2, 3, 4])
+@pytest.mark.parametrize("case", FAMILY_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_C{c[1]}")
+def test_pass_c_families_fwd_bwd(case, family):
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    grid, C, modes = case
+    v, R, W, b, dy = _problem(grid, C, modes, 1, seed=707)
+    plan = G.make_plan(grid, C, modes)
+    ran = []
+    for mode in ("fwd", "bwd"):
+        try:
+            fno.plan_set_pass_c(plan, mode, family)
+            ran.append(mode)
+        except fno.FnoError:
+            pass
+    if not ran:
+        pytest.skip(f"family {family} does not cover this shape")
+    assert {m: fno.plan_pass_c_kernels(plan)[m]["family"][:7] for m in ran}
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    y_ref, z_ref = sp.layer_fwd(G.f32(v), G.f32(R), G.f32(W), G.f32(b), modes)
+    assert rel_l2(G.np64(z), z_ref) < TOL
+    assert rel_l2(G.np64(y), y_ref) < TOL
+    dyt = G.t32(dy)
+    dv = torch.empty_like(dyt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.empty((C, C), device="cuda")
+    db = torch.empty((C,), device="cuda")
+    fno.layer_bwd(plan, G.t32(v), z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db)
+    torch.cuda.synchronize()
+    dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
+    for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
+        assert rel_l2(G.np64(got), ref) < TOL, (name, rel_l2(G.np64(got), ref))
