@@ -226,6 +226,9 @@ __global__ void __launch_bounds__(256) mix_fwd_kernel(MixParams p) {
 
 // backward mixing: W'^[b,i,m] = sum_o G^[b,o,m] conj(R[i,o,m]);
 // dR[i,o,m] (+)= (c(kt)/N) sum_b conj(V^[b,i,m]) G^[b,o,m]
+// Batch 1 (every BASELINE config): two rows i per thread, fully unrolled so
+// the R loads of the second row issue before the first row's dR stores -- the
+// R read stream and the dR write stream are in flight together.
 template <int CMAX>
 __global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
   const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -236,6 +239,41 @@ __global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
   const float cw = (kt == 0 || ((p.T & 1) == 0 && 2 * kt == p.T)) ? 1.0f : 2.0f;
   const float scale = cw * p.inv_n;
   float2 g[CMAX];
+  if (p.B == 1) {
+#pragma unroll
+    for (int o = 0; o < CMAX; ++o)
+      if (o < C) g[o] = __ldg(p.ghat + (long long)o * p.M + m);
+    float2 r[MCH][CMAX];
+#pragma unroll
+    for (int ii = 0; ii < MCH; ++ii) {
+      const int i = i0 + ii;
+#pragma unroll
+      for (int o = 0; o < CMAX; ++o)
+        if (o < C && i < C) r[ii][o] = __ldcs(p.R + ((long long)i * C + o) * p.M + m);
+    }
+#pragma unroll
+    for (int ii = 0; ii < MCH; ++ii) {
+      const int i = i0 + ii;
+      if (i >= C) continue;
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < CMAX; ++o)
+        if (o < C) acc = cfma_conj_a(r[ii][o], g[o], acc);
+      p.what[(long long)i * p.M + m] = acc;
+      if (p.dR == nullptr) continue;
+      const float2 vs = cscale(cconj(__ldg(p.vhat + (long long)i * p.M + m)), scale);
+#pragma unroll
+      for (int o = 0; o < CMAX; ++o) {
+        if (o < C) {
+          float2* d = p.dR + ((long long)i * C + o) * p.M + m;
+          float2 val = cmul(vs, g[o]);
+          if (p.accumulate) val = cadd(*d, val);
+          __stcs(d, val);
+        }
+      }
+    }
+    return;
+  }
   for (int b = 0; b < p.B; ++b) {
 #pragma unroll
     for (int o = 0; o < CMAX; ++o)
@@ -252,24 +290,6 @@ __global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
     }
   }
   if (p.dR == nullptr) return;
-  if (p.B == 1) {   // g still holds G^[0, :, m]
-#pragma unroll 1
-    for (int ii = 0; ii < MCH; ++ii) {
-      const int i = i0 + ii;
-      if (i >= C) break;
-      const float2 vs = cscale(cconj(__ldg(p.vhat + (long long)i * p.M + m)), scale);
-#pragma unroll
-      for (int o = 0; o < CMAX; ++o) {
-        if (o < C) {
-          float2* d = p.dR + ((long long)i * C + o) * p.M + m;
-          float2 val = cmul(vs, g[o]);
-          if (p.accumulate) val = cadd(*d, val);
-          __stcs(d, val);
-        }
-      }
-    }
-    return;
-  }
   for (int ii = 0; ii < MCH; ++ii) {
     const int i = i0 + ii;
     if (i >= C) break;
