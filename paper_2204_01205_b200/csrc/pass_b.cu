@@ -305,6 +305,96 @@ __global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// batched mixing (B > 1): per mode the (B x C).(C x C) complex
+// product, R read ONCE for all B batch rows.  CTA = 32 consecutive modes x 8
+// channel rows (one warp per row: 256-byte coalesced R / V^ / G^ rows); the
+// batch rows of V^ (fwd) or G^ (bwd) are re-read by the 8 warps through L1.
+// Per R element: B complex MACs (fwd), 2B (bwd: W'^ and dR) -- FFMA keeps up
+// with the R stream up to B ~ 16 at C = 20; batches beyond
+// BMAX run in chunks of BMAX, re-streaming R per chunk.
+// ---------------------------------------------------------------------------
+template <int BMAX>
+__global__ void __launch_bounds__(256) mix_fwd_batched_kernel(MixParams p, int b0, int nb) {
+  const long long m = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int o = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (m >= p.M || o >= p.C) return;
+  const int C = p.C;
+  float2 acc[BMAX];
+#pragma unroll
+  for (int b = 0; b < BMAX; ++b) acc[b] = make_float2(0.f, 0.f);
+  for (int i = 0; i < C; ++i) {
+    const float2 r = __ldcs(p.R + ((long long)i * C + o) * p.M + m);
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b)
+      if (b < nb) acc[b] = cfma(__ldg(p.vhat + ((long long)(b0 + b) * C + i) * p.M + m), r, acc[b]);
+  }
+#pragma unroll
+  for (int b = 0; b < BMAX; ++b)
+    if (b < nb) p.what[((long long)(b0 + b) * C + o) * p.M + m] = acc[b];
+}
+
+// W'^[b,i] = sum_o G^[b,o] conj(R[i,o]);  dR[i,o] (+)= (c/N) sum_b conj(V^[b,i]) G^[b,o]
+// (first chunk b0 == 0 writes or accumulates dR, later chunks add)
+template <int BMAX>
+__global__ void __launch_bounds__(256) mix_bwd_batched_kernel(MixParams p, int b0, int nb) {
+  const long long m = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (m >= p.M || i >= p.C) return;
+  const int C = p.C;
+  const int kt = int(m % p.mt);
+  const float cw = (kt == 0 || ((p.T & 1) == 0 && 2 * kt == p.T)) ? 1.0f : 2.0f;
+  const float scale = cw * p.inv_n;
+  float2 vs[BMAX], acc[BMAX];
+#pragma unroll
+  for (int b = 0; b < BMAX; ++b) {
+    acc[b] = make_float2(0.f, 0.f);
+    vs[b] = (b < nb && p.dR) ? cconj(__ldg(p.vhat + ((long long)(b0 + b) * C + i) * p.M + m)) : make_float2(0.f, 0.f);
+  }
+  for (int o = 0; o < C; ++o) {
+    const float2 r = __ldcs(p.R + ((long long)i * C + o) * p.M + m);
+    float2 d = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) {
+      if (b < nb) {
+        const float2 g = __ldg(p.ghat + ((long long)(b0 + b) * C + o) * p.M + m);
+        acc[b] = cfma_conj_a(r, g, acc[b]);
+        d = cfma(vs[b], g, d);
+      }
+    }
+    if (p.dR) {
+      float2* dp = p.dR + ((long long)i * C + o) * p.M + m;
+      float2 val = cscale(d, scale);
+      if (p.accumulate || b0 > 0) val = cadd(*dp, val);
+      __stcs(dp, val);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < BMAX; ++b)
+    if (b < nb) p.what[((long long)(b0 + b) * C + i) * p.M + m] = acc[b];
+}
+
+template <int BMAX>
+static cudaError_t launch_mix_batched(const MixParams& p, bool bwd, cudaStream_t st) {
+  const dim3 grid(unsigned((p.M + 31) / 32), unsigned((p.C + 7) / 8));
+  for (int b0 = 0; b0 < p.B; b0 += BMAX) {
+    const int nb = p.B - b0 < BMAX ? p.B - b0 : BMAX;
+    if (bwd) mix_bwd_batched_kernel<BMAX><<<grid, 256, 0, st>>>(p, b0, nb);
+    else mix_fwd_batched_kernel<BMAX><<<grid, 256, 0, st>>>(p, b0, nb);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t launch_mix_b(const MixParams& p, bool bwd, cudaStream_t st) {
+  if (p.M <= 0) return cudaSuccess;
+  if (p.B <= 2) return launch_mix_batched<2>(p, bwd, st);
+  if (p.B <= 4) return launch_mix_batched<4>(p, bwd, st);
+  if (p.B <= 8) return launch_mix_batched<8>(p, bwd, st);
+  return launch_mix_batched<16>(p, bwd, st);
+}
+
 // deterministic fixed-order column sums; columns [0, split) go to out0,
 // [split, len) to out1 (nullable)
 // (one warp per column: lane i sums rows i, i + 32, ... in ascending order, then
@@ -376,6 +466,7 @@ static cudaError_t launch_mix(K k, const MixParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 cudaError_t launch_mix_fwd(const MixParams& p, cudaStream_t st) {
+  if (p.B > 1) return launch_mix_b(p, false, st);
   if (p.C <= 4) return launch_mix(mix_fwd_kernel<4>, p, st);
   if (p.C <= 8) return launch_mix(mix_fwd_kernel<8>, p, st);
   if (p.C <= 12) return launch_mix(mix_fwd_kernel<12>, p, st);
@@ -387,6 +478,7 @@ cudaError_t launch_mix_fwd(const MixParams& p, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st) {
+  if (p.B > 1) return launch_mix_b(p, true, st);
   if (p.C <= 4) return launch_mix(mix_bwd_kernel<4>, p, st);
   if (p.C <= 8) return launch_mix(mix_bwd_kernel<8>, p, st);
   if (p.C <= 12) return launch_mix(mix_bwd_kernel<12>, p, st);

@@ -373,3 +373,33 @@ def test_pass_c_families_fwd_bwd(case, family):
     dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
     for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
         assert rel_l2(G.np64(got), ref) < TOL, (name, rel_l2(G.np64(got), ref))
+
+
+# Batched mixing: B > 1 reads R once per mode for all batch
+# rows (chunks of 16 beyond that); forward and backward vs the oracle.
+@pytest.mark.parametrize("B", [4, 8, 20])
+def test_batched_mixing_fwd_bwd(B):
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    grid, C, modes = (16, 16, 16, 8), 6, (4, 4, 4, 4)
+    v, R, W, b, dy = _problem(grid, C, modes, B, seed=808 + B)
+    plan = G.make_plan(grid, C, modes, B)
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    y_ref, z_ref = sp.layer_fwd(G.f32(v), G.f32(R), G.f32(W), G.f32(b), modes)
+    assert rel_l2(G.np64(vh), sp.forward_modes(G.f32(v), modes)) < TOL
+    assert rel_l2(G.np64(y), y_ref) < TOL
+    dyt = G.t32(dy)
+    dv = torch.empty_like(dyt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.empty((C, C), device="cuda")
+    db = torch.empty((C,), device="cuda")
+    fno.layer_bwd(plan, G.t32(v), z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db)
+    torch.cuda.synchronize()
+    dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
+    for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
+        assert rel_l2(G.np64(got), ref) < TOL, (name, rel_l2(G.np64(got), ref))
+    # accumulate adds a second dR
+    fno.layer_bwd(plan, G.t32(v), z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_l2(G.np64(dR), 2 * dR_r) < TOL
