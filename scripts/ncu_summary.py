@@ -51,7 +51,13 @@ def num(x):
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    """rep: an .ncu-rep, or the `--page raw --csv` export of one (optionally .gz)"""
+    if rep.endswith(".csv") or rep.endswith(".csv.gz"):
+        import gzip
+        out = (gzip.open(rep, "rt") if rep.endswith(".gz") else open(rep)).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     return [dict(zip(hdr, r)) for r in rows[2:]], dict(zip(hdr, units))
@@ -89,6 +95,10 @@ def summarise_rep(rep):
             smem_per_block=int(to_bytes(r.get("launch__shared_mem_per_block", 0),
                                         units.get("launch__shared_mem_per_block", "byte"))),
             warps_active_pct=num(r.get("sm__warps_active.avg.pct_of_peak_sustained_active", "nan")),
+            tensor_pipe_pct=num(r.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                                      r.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                                            "nan"))),
+            issue_active_pct=num(r.get("smsp__issue_active.avg.pct_of_peak_sustained_active", "nan")),
             top_stalls=[(k, round(100 * v / tot, 1)) for v, k in st[:5]]))
     return res
 
@@ -125,12 +135,14 @@ def main():
         ks = summarise_rep(a.rep)
         json.dump(ks, open(os.path.join(a.out, "ncu_full_summary.json"), "w"), indent=1)
         md.append("## ncu --set full (one launch per kernel)\n")
-        md.append("| stage | us | DRAM MB (r+w) | DRAM GB/s | DRAM % | SM % | regs | smem KB | grid x block | top stalls |")
-        md.append("|---|---|---|---|---|---|---|---|---|---|")
+        md.append("| stage | us | DRAM MB (r+w) | DRAM GB/s | DRAM % | SM % | issue % | tensor % | warps % | regs | "
+                  "smem KB | grid x block | top stalls |")
+        md.append("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
         for k in ks:
             stalls = ", ".join(f"{n} {p}%" for n, p in k["top_stalls"][:3])
             md.append(f"| {k['stage']} | {k['duration_us']} | {k['dram_bytes'] / 1e6:.1f} | {k['dram_gbs']} | "
-                      f"{k['dram_pct_peak']:.1f} | {k['sm_pct_peak']:.1f} | {k['registers']} | "
+                      f"{k['dram_pct_peak']:.1f} | {k['sm_pct_peak']:.1f} | {k['issue_active_pct']:.1f} | "
+                      f"{k['tensor_pipe_pct']:.2f} | {k['warps_active_pct']:.1f} | {k['registers']} | "
                       f"{k['smem_per_block'] / 1024:.1f} | {k['grid']} x {k['block']} | {stalls} |")
         if a.traffic:
             allt = json.load(open(a.traffic)) if os.path.exists(a.traffic) else {}
