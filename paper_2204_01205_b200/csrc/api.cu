@@ -408,7 +408,7 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   p->o_dwloc = take(dwlen * 4);
   p->o_dwall = take(size_t(P) * dwlen * 4);
   p->o_dz = take(size_t(p->B) * p->C * p->Xl * p->Yl * p->Z * p->T * 4);   // dz = dy * sigma'(z) (bwd)
-  p->o_bar = take(256);                      // peer-exchange barrier word
+  p->o_bar = take(1024);                     // peer-exchange barrier: flag row [64] + epoch (zeroed at connect)
   p->o_ipc = take(size_t(P) * 256);          // peer-exchange handle all-gather
   p->total = off;
   *out = p;
@@ -481,6 +481,9 @@ extern "C" fno_status fno_plan_connect_peers(fno_plan_t p, void* stream) {
     cudaGetLastError();
   }
   unsigned char* dbuf = static_cast<unsigned char*>(p->ws) + p->o_ipc;
+  // barrier flag rows start at epoch 0 on every rank before any rank can write
+  // into a peer's row (the handle all-gather below orders the two)
+  FNO_CUDA(cudaMemsetAsync(static_cast<char*>(p->ws) + p->o_bar, 0, 1024, st), "peer barrier flags");
   FNO_CUDA(cudaMemcpyAsync(dbuf + size_t(p->rank) * 256, &mine, sizeof mine, cudaMemcpyHostToDevice, st), "ipc h2d");
   FNO_NCCL(ncclAllGather(dbuf + size_t(p->rank) * 256, dbuf, 256, ncclUint8, p->comm->nccl, st), "ipc all-gather");
   std::vector<unsigned char> all(size_t(p->P) * 256);
@@ -641,9 +644,14 @@ PassBParams make_b(fno_plan_t p, const float2* in, float2* out, int Q) {
 // y-inverse; the exchange is a barrier (one-int NCCL all-reduce), after which
 // every rank's receive buffer is complete (writers fenced at system scope)
 fno_status peer_barrier(fno_plan_t p, int stage, const char* what, cudaStream_t st) {
-  StageScope sc(p, stage, st);
-  int* w = wsp<int>(p, p->o_bar);
-  FNO_NCCL(ncclAllReduce(w, w, 1, ncclInt, ncclSum, p->comm->nccl, st), what);
+  // flag rows at o_bar: [0, 64) flags (u64 per source rank), [64] the epoch
+  PeerBarrierParams b{};
+  b.P = p->P;
+  b.rank = p->rank;
+  b.my_flags = wsp<unsigned long long>(p, p->o_bar);
+  b.epoch = b.my_flags + FNO_MAXP;
+  for (int d = 0; d < p->P; ++d) b.peer_flags[d] = reinterpret_cast<unsigned long long*>(p->peer_ws[d] + p->o_bar);
+  FNO_LAUNCH(p, stage, launch_peer_barrier(b, st), what);
   return FNO_OK;
 }
 

@@ -101,6 +101,15 @@ cudaError_t launch_rowsum_strided(const float* rows, int nrows, long long stride
 cudaError_t launch_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
                         float eps, int step, int num_sms, cudaStream_t st);
 
+// exchange barrier over NVLink peer memory (peer.cu)
+struct PeerBarrierParams {
+  unsigned long long* peer_flags[FNO_MAXP];   // rank d's flag row (mapped over NVLink); this rank writes [rank]
+  unsigned long long* my_flags;               // this rank's row: [d] = rank d's latest arrival epoch
+  unsigned long long* epoch;                  // this rank's barrier count
+  int P, rank;
+};
+cudaError_t launch_peer_barrier(const PeerBarrierParams& p, cudaStream_t st);
+
 bool ac_pair_supported(int LZ, int LT);
 bool b_size_supported(int L);
 
