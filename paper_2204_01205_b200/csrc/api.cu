@@ -551,6 +551,15 @@ extern "C" fno_status fno_plan_set_pass_c(fno_plan_t p, int mode, int family) {
   return FNO_OK;
 }
 
+#ifdef FNO_C4_PROFILE
+// development builds: the pass_c4 role timers of the last pass C launch ([grid][16] u64 in the pass B scratch H)
+extern "C" fno_status fno_debug_c4_timers(fno_plan_t p, unsigned long long* host, int n) {
+  if (!p || !host || !p->ws) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_debug_c4_timers");
+  FNO_CUDA(cudaMemcpy(host, static_cast<char*>(p->ws) + p->o_h, size_t(n) * 8, cudaMemcpyDeviceToHost), "timers");
+  return FNO_OK;
+}
+#endif
+
 extern "C" fno_status fno_plan_local_box(fno_plan_t p, int64_t lo[4], int64_t hi[4]) {
   if (!p || !lo || !hi) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_local_box: NULL argument");
   lo[0] = p->ix * p->Xl; hi[0] = lo[0] + p->Xl;
@@ -753,7 +762,10 @@ PassCParams make_c(fno_plan_t p, int mode) {
   }
 #endif
   c.in = wsp<float2>(p, p->o_slab_xy);
-  c.dWpart = wsp<float>(p, p->o_dwpart);   // bwd: dW / db partial rows (profiling builds: role timers)
+  c.dWpart = wsp<float>(p, p->o_dwpart);   // bwd: dW / db partial rows
+#ifdef FNO_C4_PROFILE
+  c.prof = wsp<unsigned long long>(p, p->o_h);   // development builds: pass_c4 role timers
+#endif
   c.n_cols = (long long)p->B * p->Xl * p->Yl;
   c.B = p->B; c.C = p->C; c.Xl = int(p->Xl); c.Yl = int(p->Yl); c.Z = int(p->Z); c.T = int(p->T);
   c.mz = p->mz; c.mt = p->mt; c.Qz = p->Qz; c.Qt = p->Qt;

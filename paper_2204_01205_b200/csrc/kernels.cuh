@@ -79,6 +79,7 @@ struct PassCParams {
   int use_tma;          // pass_c2/c3: tile inputs by TMA tensor maps (c2_tile_group > 0)
   int tma_g;            // z rows per TMA row group (1: T % 4 == 0; 2: T % 4 == 2; 4: T odd)
   int NX;               // pass_c2: X tile buffers (1 or 2)
+  unsigned long long* prof;   // development builds (FNO_C4_PROFILE): pass_c4 role timers, [grid][16]
   int ablate;           // profiling only (FNO_ABLATE): bit 0 skip phase 2, bit 1 skip 1x1, bit 2 skip stores, bit 3 skip dW, bit 4 skip phase 1
   int act_gelu;         // 1: sigma = GELU, 0: identity
   float inv_n;          // 1 / (X Y Z T)

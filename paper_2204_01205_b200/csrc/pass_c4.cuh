@@ -129,16 +129,15 @@ __host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, in
 }
 
 // Development builds (-DFNO_C4_PROFILE, scripts/variant_libs.sh): per-CTA
-// clock64 timers of each role's waits and work, written over the (forward-
-// unused) dW partial rows: slot i of CTA b at ((u64*)p.dWpart)[16 b + i].
+// clock64 timers of each role's waits and work: slot i of CTA b at p.prof[16 b + i]
+// (the pass B scratch H, unused during pass C).
 #ifdef FNO_C4_PROFILE
 #define C4P_DECL unsigned long long c4p[16] = {0};
 #define C4P_T(v) const long long v = clock64();
 #define C4P_ADD(slot, v) c4p[slot] += (unsigned long long)(clock64() - (v));
 #define C4P_DUMP(cond, first, n)                                                               \
-  if ((cond) && EPI != EPI_BWD)                                                                \
-    for (int i_ = 0; i_ < (n); ++i_)                                                           \
-      reinterpret_cast<unsigned long long*>(p.dWpart)[16ll * blockIdx.x + (first) + i_] = c4p[(first) + i_];
+  if ((cond) && p.prof)                                                                        \
+    for (int i_ = 0; i_ < (n); ++i_) p.prof[16ll * blockIdx.x + (first) + i_] = c4p[(first) + i_];
 #else
 #define C4P_DECL
 #define C4P_T(v)

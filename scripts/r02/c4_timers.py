@@ -21,8 +21,17 @@ R = torch.from_numpy(synth.spectral_weights(C, C, modes, 2)).cuda()
 W, b = [torch.from_numpy(a).cuda() for a in synth.channel_weights(C, 3)]
 y, z = torch.empty_like(v), torch.empty_like(v)
 vh = torch.empty(plan.vhat_shape(), dtype=torch.complex64, device="cuda")
+mode = sys.argv[2] if len(sys.argv) > 2 else "fwd"
+fno.plan_set_pass_c(plan, mode, 4)
 for _ in range(3):
     fno.layer_fwd(plan, v, R, W, b, y, z, vh)
+if mode == "bwd":
+    dv = torch.empty_like(v)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.empty((C, C), device="cuda")
+    db = torch.empty((C,), device="cuda")
+    for _ in range(3):
+        fno.layer_bwd(plan, v, z, vh, torch.randn_like(v), R, W, dv, dR, dW, db)
 torch.cuda.synchronize()
 L = fno.lib()
 L.fno_debug_c4_timers.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
