@@ -348,7 +348,8 @@ def plan_pass_c_kernels(plan: Plan) -> dict:
         out[name] = {"family": fam.get(info[0], info[0]), "width": info[1], "stages": info[2] & 255,
                      "smem": info[3]}
         if info[0] == 4 and info[2] >> 8:
-            out[name]["u_buffers"] = info[2] >> 8
+            out[name]["u_buffers"] = (info[2] >> 8) & 255
+            out[name]["slab_staged"] = bool((info[2] >> 16) & 1)
     return out
 
 

@@ -23,25 +23,34 @@ static int c4_cp_of(int C) {
 // deepest input ring that fits 227 KB (forward up to 6 stages, backward up to
 // 4; at least 2, else the plan keeps pass_c2 / pass_c3)
 bool pass_c4_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* CPo, int* NS, size_t* smem) {
-  (void)mt;
   const int CP = c4_cp_of(C);
   if (!CP) return false;
   if (LZ != 8 && LZ != 16 && LZ != 32) return false;
   if (128 / LZ > T) return false;
   const size_t cap = 227 * 1024;
-  if (mode == EPI_U) {
-    const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, 1).total;
-    if (s > cap) return false;
-    *CPo = CP; *NS = 1; *smem = s;
-    return true;
-  }
-  // preference: four U buffers with an input ring of >= 3 stages, then two U
-  // buffers with the deepest ring (>= 2)
-  for (int nub : {4, 2}) {
-    for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= (nub == 4 ? 3 : 2); --ns) {
-      const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, ns, nub).total;
+  if (mode == EPI_U) {   // no input tiles; the slab staged when it fits
+    for (int sl = (C * mt) % 2 == 0 ? 1 : 0; sl >= 0; --sl) {
+      const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, 1, 2, sl, mt).total;
       if (s <= cap) {
-        *CPo = CP; *NS = ns | (nub << 8); *smem = s;
+        *CPo = CP; *NS = 1 | (2 << 8) | (sl << 16); *smem = s;
+        return true;
+      }
+    }
+    return false;
+  }
+  // preference: the column slab staged by TMA (phase 1 off L2) with four U
+  // buffers and >= 3 ring stages, staged with two U buffers, then unstaged with
+  // four / two U buffers and the deepest ring.  Staging needs 16-byte bulk
+  // copies: C mt even (every chunk size and offset a multiple of 16 bytes).
+  const bool sl_ok = (C * mt) % 2 == 0;
+  struct Pref { int sl, nub, nsmin; };
+  const Pref prefs[] = {{1, 4, 3}, {1, 2, 3}, {0, 4, 3}, {0, 2, 2}};
+  for (const Pref& pr : prefs) {
+    if (pr.sl && !sl_ok) continue;
+    for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= pr.nsmin; --ns) {
+      const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, ns, pr.nub, pr.sl, mt).total;
+      if (s <= cap) {
+        *CPo = CP; *NS = ns | (pr.nub << 8) | (pr.sl << 16); *smem = s;
         return true;
       }
     }

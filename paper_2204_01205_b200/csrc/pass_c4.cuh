@@ -71,18 +71,21 @@ __host__ __device__ constexpr int c4_tmem_cols(int CP, int mode) {
 }
 
 struct C4Layout {
-  int NS, NUB, NOB, KP, NP, NW, RG, nk, TP, UPS;
-  size_t x, xstage, op, opstage, a1hi, a1lo, a2hi, a2lo, b2hi, b2lo, b1hi, b1lo, bb, u0, ustride, twz, twt, dmap, bar, slot,
+  int NS, NUB, NOB, SL, KP, NP, NW, RG, nk, TP, UPS;
+  size_t x, xstage, op, opstage, a1hi, a1lo, a2hi, a2lo, b2hi, b2lo, b1hi, b1lo, bb, u0, ustride, sl, twz, twt, dmap, bar, slot,
       red, total;
 };
 
 // NS: input-tile ring stages; NUB: U buffers (2, or 4 = two per epilogue
 // warpgroup, so the transforms run a tile further ahead); operand buffers: 2
 // (fwd), 1 (bwd)
+// SL: the column's slab staged in shared memory by a TMA bulk copy (issued by
+// the producer one column ahead), so phase 1 reads shared memory, not L2
 __host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, int T, int mz, int LZ, int NS,
-                                              int NUB = 2) {
+                                              int NUB = 2, int SL = 0, int mt = 0) {
   C4Layout L{};
   L.NUB = NUB;
+  L.SL = SL;
   const bool bwd = mode == EPI_BWD, mma = mode != EPI_U;
   L.NS = mma ? NS : 0;
   L.NOB = mode == EPI_FWD ? 2 : (bwd ? 1 : 0);
@@ -117,11 +120,12 @@ __host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, in
   L.bb = take(size_t(C) * L.nk * L.TP * sizeof(float2));
   L.ustride = (size_t(C) * L.UPS * sizeof(float) + 1023) & ~size_t(1023);
   L.u0 = take(L.ustride * NUB);
+  L.sl = take(SL ? size_t(C) * 2 * mz * mt * sizeof(float2) : 0);
   auto take16 = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
   L.twz = take16(size_t(Z) * sizeof(float2));
   L.twt = take16(size_t(T) * sizeof(float2));
   L.dmap = take16(size_t(2 * mz) * sizeof(short2));
-  L.bar = take16(32 * sizeof(uint64_t));
+  L.bar = take16(40 * sizeof(uint64_t));
   L.slot = take16(sizeof(uint32_t));
   L.red = take16(bwd ? size_t(2) * 32 * L.NW * sizeof(float) : 16);   // dW / db sums of the two warpgroups
   L.total = off;
@@ -168,8 +172,10 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int C = p.C, Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
   const int NS = MMA ? (p.NX & 255) : 1;
-  const int NUB = (p.NX >> 8) == 4 ? 4 : 2;
-  const C4Layout L = c4_layout(CP, EPI, C, Z, T, mz, LZ, NS, NUB);
+  const int NUB = ((p.NX >> 8) & 255) == 4 ? 4 : 2;
+  const bool SL = (p.NX >> 16) & 1;
+  const C4Layout L = c4_layout(CP, EPI, C, Z, T, mz, LZ, NS, NUB, SL ? 1 : 0, mt);
+  const float2* sl = reinterpret_cast<const float2*>(smem_raw + L.sl);
   float2* Bb = reinterpret_cast<float2*>(smem_raw + L.bb);
   float2* twZ = reinterpret_cast<float2*>(smem_raw + L.twz);
   float2* twT = reinterpret_cast<float2*>(smem_raw + L.twt);
@@ -183,6 +189,8 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
   uint64_t* dempty = bars + 22;    // [2]   4 epilogue warps read D[b]
   uint64_t* ufull = bars + 24;     // [NUB] 6 transform warps wrote U[k % NUB]
   uint64_t* uempty = bars + 28;    // [NUB] 4 epilogue warps read U[k % NUB]
+  uint64_t* slfull = bars + 32;    // [1]   the column's slab landed (SL)
+  uint64_t* slempty = bars + 33;   // [1]   6 transform warps finished phase 1 (SL)
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem_raw + L.slot);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk = L.nk, TP = L.TP, UPS = L.UPS;
@@ -261,6 +269,8 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
       mbar_init(&dfull[b], 1);
       mbar_init(&dempty[b], 4);
     }
+    mbar_init(slfull, 1);
+    mbar_init(slempty, C4_NTT / 32);
     for (int b = 0; b < NUB; ++b) {
       mbar_init(&ufull[b], C4_NTT / 32);
       mbar_init(&uempty[b], 4);
@@ -292,13 +302,26 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
 
   if (warp == C4_PROD) {
     // ======================= TMA producer ========================================
-    if (MMA && lane == 0) {
+    if ((MMA || SL) && lane == 0) {
       C4P_DECL
       int s = 0;
       unsigned xph = 0;   // parity of the ring's current pass
-      for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
+      unsigned ci = 0;    // column count (slab parity)
+      for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x, ++ci) {
         int bb;
         const int xy = col_split(col, &bb);
+        if (SL) {   // the column's slab, one bulk copy per kz owner chunk (stacked in owner order)
+          mbar_wait(slempty, (ci & 1u) ^ 1u);
+          mbar_expect_tx(slfull, unsigned(C) * 2 * mz * mt * sizeof(float2));
+          for (int d = 0; d < p.slab.P; ++d) {
+            const int nkz_d = p.slab.kz_lo[d + 1] - p.slab.kz_lo[d];
+            if (nkz_d == 0) continue;
+            const unsigned bytes = unsigned(C) * nkz_d * mt * sizeof(float2);
+            tma_load_1d(const_cast<float2*>(sl) + (long long)C * mt * p.slab.kz_lo[d],
+                        p.in + p.slab.off[d] + col * C * nkz_d * mt, bytes, slfull);
+          }
+        }
+        if (!MMA) continue;
         int rz = 0, tc = 0;
         for (int ti = 0; ti < tpc; ++ti, next_tile(rz, tc)) {
           C4P_T(tw0)
@@ -377,6 +400,14 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
   } else if (warp == 6 || warp == 7 || warp >= 12) {
     // ======================= transforms (phases 1-2) ===============================
     const int ttid = (warp < 8 ? warp - 6 : warp - 10) * 32 + lane;
+    // staged slab (SL): chunk d at C mt kz_lo[d], rows (c, jz - kz_lo[d]) of that chunk
+    // (an offset into the shared array, so the loads stay LDS)
+    auto sl_off = [&](int c, int jz) -> int {
+      if (p.slab.P == 1) return (c * 2 * mz + jz) * mt;
+      const short2 dm = dmap[jz];
+      const int nkz = p.slab.kz_lo[dm.x + 1] - p.slab.kz_lo[dm.x];
+      return C * mt * p.slab.kz_lo[dm.x] + (c * nkz + dm.y) * mt;
+    };
     auto slab_at = [&](long long c_, int c, int jz) -> const float2* {
       if (p.slab.P == 1) return p.in + (c_ * C + c) * per_c + jz * mt;
       const short2 dm = dmap[jz];
@@ -384,30 +415,33 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
       return p.in + p.slab.off[dm.x] + ((c_ * C + c) * nkz + dm.y) * mt;
     };
     C4P_DECL
-    unsigned k = 0;
-    for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x) {
+    unsigned k = 0, ci = 0;
+    for (long long col = blockIdx.x; col < p.n_cols; col += gridDim.x, ++ci) {
       const long long col_next = col + gridDim.x;
       C4P_T(tp1)
       group_sync(2, C4_NTT);   // the previous column's phase 2 is done with Bb
+      if (SL) mbar_wait(slfull, ci & 1u);   // this column's slab in shared memory
       // ---- phase 1: inverse t (C2R weights and 1/N folded in), items (c, kz', rt)
       for (int it = ttid; it < C * nk * p.Qt; it += C4_NTT) {
         const int rt = it % p.Qt;
         const int pid = it / p.Qt;
         const int c = pid / nk, kzp = pid - c * nk;
-        const float2* Sp = slab_at(col, c, kzp < mz ? kzp : 0);
-        const float2* Sn = slab_at(col, c, kzp >= 1 ? 2 * mz - kzp : 0);
+        const int jzp = kzp < mz ? kzp : 0, jzn = kzp >= 1 ? 2 * mz - kzp : 0;
+        const float2* Sp = SL ? nullptr : slab_at(col, c, jzp);
+        const float2* Sn = SL ? nullptr : slab_at(col, c, jzn);
+        const int op = SL ? sl_off(c, jzp) : 0, on = SL ? sl_off(c, jzn) : 0;
         float2 e[LT];
 #pragma unroll
         for (int i = 0; i < LT; ++i) {
           float2 acc = make_float2(0.f, 0.f);
           if (i < mt && kzp < mz) {
             const float cw = (i == 0 || 2 * i == T) ? 1.f : 2.f;
-            acc = cscale(__ldg(Sp + i), cw);
+            acc = cscale(SL ? sl[op + i] : __ldg(Sp + i), cw);
           }
           const int kt = (LT - i) % LT;
           if (kzp >= 1 && kt < mt && (i == 0 || i > LT - mt)) {
             const float cw = (kt == 0 || 2 * kt == T) ? 1.f : 2.f;
-            acc = cadd(acc, cscale(cconj(__ldg(Sn + kt)), cw));
+            acc = cadd(acc, cscale(cconj(SL ? sl[on + kt] : __ldg(Sn + kt)), cw));
           }
           e[i] = acc;
         }
@@ -418,8 +452,9 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
         for (int s = 0; s < LT; ++s) bo[p.Qt * s] = cscale(y[s], p.inv_n);   // the 1/N of the inverse
       }
       group_sync(2, C4_NTT);   // Bb complete
+      if (SL && lane == 0) mbar_arrive(slempty);   // the staged slab may be refilled
       C4P_ADD(8, tp1)
-      if (col_next < p.n_cols)   // next column's slab rows into L1 (phase 1 then hits L1)
+      if (!SL && col_next < p.n_cols)   // next column's slab rows into L1 (phase 1 then hits L1)
         for (int r = ttid; r < C * 2 * mz; r += C4_NTT)
           asm volatile("prefetch.global.L1 [%0];" ::"l"(slab_at(col_next, r / (2 * mz), r % (2 * mz))));
       int rz = 0, tc = 0;
