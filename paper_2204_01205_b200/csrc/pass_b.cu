@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) mix_fwd_kernel(MixParams p) {
 // the R loads of the second row issue before the first row's dR stores -- the
 // R read stream and the dR write stream are in flight together.
 template <int CMAX>
-__global__ void __launch_bounds__(256) mix_bwd_kernel(MixParams p) {
+__global__ void __launch_bounds__(256, 2) mix_bwd_kernel(MixParams p) {
   const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= p.M) return;
   const int C = p.C;

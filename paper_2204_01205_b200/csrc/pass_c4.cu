@@ -44,7 +44,7 @@ bool pass_c4_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   // copies: C mt even (every chunk size and offset a multiple of 16 bytes).
   const bool sl_ok = (C * mt) % 2 == 0;
   struct Pref { int sl, nub, nsmin; };
-  const Pref prefs[] = {{1, 4, 3}, {1, 2, 3}, {0, 4, 3}, {0, 2, 2}};
+  const Pref prefs[] = {{1, 4, 3}, {1, 4, 2}, {1, 2, 3}, {0, 4, 3}, {0, 2, 2}};
   for (const Pref& pr : prefs) {
     if (pr.sl && !sl_ok) continue;
     for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= pr.nsmin; --ns) {
