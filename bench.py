@@ -711,7 +711,8 @@ def run_reference(args, rank, world):
         "dtype": "f64",
         "data": f"synthetic (seeded {'CO2' if cfg['shape'] == 'co2' else 'NS'}-shaped fields, random-init weights)",
         "config": {"workload": WORKLOADS[cfg["name"]] + f"; oracle sample per step: one DFNO block fwd+bwd at width "
-                               f"{C} on the x/y sub-box {[xs, ys, Z, T]} of the per-GPU grid {[lx, ly, Z, T]}",
+                               f"{C} on an x/y box {[xs, ys, Z, T]} (per-GPU grid {[lx, ly, Z, T]}; the box is at "
+                               f"least 2m wide, the oracle's retained-mode limit)",
                    "global_grid": list(cfg["grid"]), "sample_grid": [xs, ys, Z, T], "width": C,
                    "modes": list(modes), "batch": 1},
         "cpu_baseline": cpu,
