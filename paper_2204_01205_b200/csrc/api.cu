@@ -398,6 +398,9 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   const size_t dwlen = size_t(p->C) * p->C + p->C;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  // the peer-exchange barrier rows first: ranks write into each other's rows at
+  // their OWN offset, so it must not depend on rank-specific sizes (nkz)
+  p->o_bar = take(1024);                     // flag row [64] + epoch (zeroed at connect)
   p->o_slab_xy = take(p->n_slab_xy * 8);
   p->o_slab_kz = (P == 1) ? p->o_slab_xy : take(p->n_slab_kz * 8);
   p->o_h = take(p->n_h * 8);
@@ -408,7 +411,6 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   p->o_dwloc = take(dwlen * 4);
   p->o_dwall = take(size_t(P) * dwlen * 4);
   p->o_dz = take(size_t(p->B) * p->C * p->Xl * p->Yl * p->Z * p->T * 4);   // dz = dy * sigma'(z) (bwd)
-  p->o_bar = take(1024);                     // peer-exchange barrier: flag row [64] + epoch (zeroed at connect)
   p->o_ipc = take(size_t(P) * 256);          // peer-exchange handle all-gather
   p->total = off;
   *out = p;
