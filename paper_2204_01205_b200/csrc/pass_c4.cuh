@@ -16,7 +16,9 @@
 // tile k-1 all proceed at once on one SM:
 //
 //   warp  4      TMA producer: NS-stage ring of input tiles X (v, or dz and v),
-//                one 5-D tensor-map box per input (c2_encode_tile_map)
+//                one 5-D tensor-map box per input (c2_encode_tile_map), and
+//                (when it fits) the next column's retained-mode slab by 1-D
+//                bulk copies, so phase 1 reads shared memory instead of L2
 //   warp  5      TMEM owner and MMA issuer (one thread): kind::tf32 3xTF32
 //                  D1[p][n]  = sum_k A1[p][k] B1[n][k]   (M128 x N NP x K KP)
 //                    fwd: A1 = v^T | 1, B1 = W | b;  bwd: A1 = dz^T, B1 = W^T
@@ -148,11 +150,6 @@ __host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, in
 #define C4P_ADD(slot, v)
 #define C4P_DUMP(cond, first, n)
 #endif
-
-// K-major (SWIZZLE_NONE) element offset, RGS row groups of 8 rows per K group of 4
-__device__ __forceinline__ int kmaj_rows(int row, int k, int RGS) {
-  return ((k >> 2) * RGS + (row >> 3)) * 32 + (row & 7) * 4 + (k & 3);
-}
 
 template <int LZ, int LT, int CP, int EPI, bool HALF, bool RAG>
 __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__ C2Maps maps, const PassCParams p) {
