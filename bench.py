@@ -162,7 +162,10 @@ def stage_bytes(prob, plan_info):
         "bwd.mix": 2 * Rb + 3 * mode,                        # R, dR, V^, G^, W'^
         "bwd.b_x_inv": mode + H,
         "bwd.b_y_inv": H + slab_kz,
-        "bwd.pass_c": slab + 8 * n + 4 * n,                  # slab, dz, v -> dv
+        # slab, dz, v -> dv; the split backward (pass C family 5): slab, dz -> dv,
+        # then dw_partial reads dz, v (its rows are "bwd.dw")
+        "bwd.pass_c": slab + 8 * n + (0 if plan_info.get("split_bwd") else 4 * n),
+        "bwd.dw": 8 * n,
         "fwd.exchange_1": slab * (P - 1) / P, "fwd.exchange_2": slab * (P - 1) / P,
         "bwd.exchange_1": slab * (P - 1) / P, "bwd.exchange_2": slab * (P - 1) / P,
     }
@@ -546,7 +549,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = units / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant kernel -----------------------------------
-    info = dict(nkz=kz_hi - kz_lo)
+    info = dict(nkz=kz_hi - kz_lo, split_bwd=plan_kernels(plan).get("bwd", {}).get("family", "").startswith("split"))
     prob = dict(B=B, C=C, local=local[2:], grid=grid, modes=modes, P=world)
     sb = stage_bytes(prob, info)
     kern = {k: v for k, v in prof.items() if "exchange" not in k and k in sb}

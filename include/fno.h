@@ -130,8 +130,12 @@ fno_status fno_plan_connect_peers(fno_plan_t plan, void* stream);
  * forward), 2 (layer backward): info = {family, padded width, input-ring
  * stages / tile buffers, dynamic shared memory bytes}; family 4 = the
  * warp-specialised tcgen05 kernel (pass_c4), 3 = pass_c3, 2 = pass_c2 (FFMA),
- * 1 = the generic pass_c.  The family-4 launch falls back to the next family
- * when the tensors' alignment rules out its TMA view. */
+ * 1 = the generic pass_c; 5 (mode 2 only, C <= 20) = the split backward: dv =
+ * W^T dz + S^T dz by the mode-1 family's kernel run with W^T, no bias and the
+ * identity (info describes that kernel), then dW and db by the streaming
+ * dw_partial kernel over dz and v (8 B per point-channel, fixed-order sums).
+ * The family-4 launch falls back to the next family when the tensors'
+ * alignment rules out its TMA view. */
 fno_status fno_plan_pass_c_info(fno_plan_t plan, int mode, int64_t info[4]);
 /* Selects the pass C kernel family (as in fno_plan_pass_c_info) for mode 0
  * (spectral u), 1 (layer forward) or 2 (layer backward).  fno_plan_create

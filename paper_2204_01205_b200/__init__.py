@@ -339,7 +339,8 @@ class Plan:
 
 def plan_pass_c_kernels(plan: Plan) -> dict:
     """{mode: {family, width, stages, smem}} of the pass C kernels the plan selected."""
-    fam = {4: "pass_c4 (warp-specialised, TMA ring, tcgen05)", 3: "pass_c3 (tcgen05 1x1)", 2: "pass_c2 (FFMA)",
+    fam = {5: "split (dv: the forward kernel with W^T; dW, db: dw_partial)",
+           4: "pass_c4 (warp-specialised, TMA ring, tcgen05)", 3: "pass_c3 (tcgen05 1x1)", 2: "pass_c2 (FFMA)",
            1: "pass_c (generic)"}
     out = {}
     for m, name in enumerate(("u", "fwd", "bwd")):
@@ -347,14 +348,17 @@ def plan_pass_c_kernels(plan: Plan) -> dict:
         _check(lib().fno_plan_pass_c_info(plan.handle, m, info), "fno_plan_pass_c_info")
         out[name] = {"family": fam.get(info[0], info[0]), "width": info[1], "stages": info[2] & 255,
                      "smem": info[3]}
-        if info[0] == 4 and info[2] >> 8:
+        if info[0] == 5:   # the configuration of its dv kernel (the forward family's)
+            out[name]["dv_kernel"] = out["fwd"]["family"]
+        if info[0] in (4, 5) and info[2] >> 8:
             out[name]["u_buffers"] = (info[2] >> 8) & 255
             out[name]["slab_staged"] = bool((info[2] >> 16) & 1)
     return out
 
 
 def plan_set_pass_c(plan: Plan, mode: str, family: int):
-    """Force the pass C kernel family (1 pass_c, 2 pass_c2, 3 pass_c3, 4 pass_c4) for mode "u" / "fwd" / "bwd"
+    """Force the pass C kernel family (1 pass_c, 2 pass_c2, 3 pass_c3, 4 pass_c4; 5 the split backward:
+    dv by the forward family's kernel with W^T, dW / db by dw_partial) for mode "u" / "fwd" / "bwd"
     (A/B runs and tests; the plan's default is the measured-fastest eligible family)."""
     m = {"u": 0, "fwd": 1, "bwd": 2}[mode]
     _check(lib().fno_plan_set_pass_c(plan.handle, m, int(family)), "fno_plan_set_pass_c")

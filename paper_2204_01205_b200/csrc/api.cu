@@ -63,10 +63,10 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-enum Stage { ST_PASS_A, ST_EX1, ST_B_YF, ST_B_XF, ST_MIX, ST_B_XI, ST_B_YI, ST_EX2, ST_PASS_C, ST_DW, ST_N };
+enum Stage { ST_PASS_A, ST_EX1, ST_B_YF, ST_B_XF, ST_MIX, ST_B_XI, ST_B_YI, ST_EX2, ST_PASS_C, ST_DWP, ST_DW, ST_N };
 static const char* kStageNames[2 * ST_N] = {
-    "fwd.pass_a", "fwd.exchange_1", "fwd.b_y_fwd", "fwd.b_x_fwd", "fwd.mix", "fwd.b_x_inv", "fwd.b_y_inv", "fwd.exchange_2", "fwd.pass_c", "fwd.unused",
-    "bwd.pass_a", "bwd.exchange_1", "bwd.b_y_fwd", "bwd.b_x_fwd", "bwd.mix", "bwd.b_x_inv", "bwd.b_y_inv", "bwd.exchange_2", "bwd.pass_c", "bwd.dw_reduce"};
+    "fwd.pass_a", "fwd.exchange_1", "fwd.b_y_fwd", "fwd.b_x_fwd", "fwd.mix", "fwd.b_x_inv", "fwd.b_y_inv", "fwd.exchange_2", "fwd.pass_c", "fwd.unused_dw", "fwd.unused",
+    "bwd.pass_a", "bwd.exchange_1", "bwd.b_y_fwd", "bwd.b_x_fwd", "bwd.mix", "bwd.b_x_inv", "bwd.b_y_inv", "bwd.exchange_2", "bwd.pass_c", "bwd.dw", "bwd.dw_reduce"};
 
 static std::atomic<unsigned long long> g_launches{0};
 
@@ -105,6 +105,10 @@ struct fno_plan_s {
   };
   KCfg kc[4][3];
   int fam[3] = {1, 1, 1};                      // the family each mode launches (fno_plan_set_pass_c)
+  // family 5 (backward only): split backward, dv = W^T dz + S^T dz by the
+  // forward-mode kernel of fam[EPI_FWD] (W^T, no bias, identity), dW / db by the
+  // streaming dw_partial kernel (dw.cu) over dz and v; dw_grid CTAs, C <= 20
+  int dw_grid = 0;
   long long mloc = 0;      // owned modes: 4 mx my nkz mt
   // workspace (bytes offsets)
   void* ws = nullptr;
@@ -346,18 +350,22 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   }
   // default choice, by measurement on B200 (profiles/r02/ab_pass_c.md): the
   // spectral u path on pass_c4; the layer forward on pass_c3 where it tiles T
-  // (T % 4 == 0), else pass_c4 (c3: 1.28 vs 1.37 ms); the layer backward on the
-  // FFMA pass_c2 (c2: 0.80 vs 2.05 ms for the tcgen05 pass_c4 backward, whose
-  // three operand splits and single-buffered operands serialise the tile pipeline)
-  auto ok = [&](int f, int m) { return p->kc[f - 1][m].cp > 0; };
+  // (T % 4 == 0), else pass_c4 (c3: 1.28 vs 1.37 ms); the layer backward split
+  // (family 5: dv by the forward kernel, dW / db by dw_partial) where T % 4 != 0,
+  // whose ragged t chunks cost the fused pass_c2 backward a zero fill of both
+  // tiles per chunk (c3: 1.94 vs 2.08 ms per layer backward), else the FFMA
+  // pass_c2 (c2: 1.31 vs 1.33, c4: 5.59 vs 5.67 ms split; 0.80 vs 2.05 ms for
+  // the tcgen05 pass_c4 backward, whose three operand splits and
+  // single-buffered operands serialise the tile pipeline)
+  auto ok = [&](int f, int m) { return f == 5 ? (m == EPI_BWD && p->C <= 20) : p->kc[f - 1][m].cp > 0; };
   p->fam[EPI_U] = ok(4, EPI_U) ? 4 : 1;
   p->fam[EPI_FWD] = (ok(3, EPI_FWD) && p->T % 4 == 0) ? 3 : ok(4, EPI_FWD) ? 4 : ok(3, EPI_FWD) ? 3 : ok(2, EPI_FWD) ? 2 : 1;
-  p->fam[EPI_BWD] = ok(2, EPI_BWD) ? 2 : ok(4, EPI_BWD) ? 4 : 1;
+  p->fam[EPI_BWD] = (ok(5, EPI_BWD) && p->T % 4 != 0) ? 5 : ok(2, EPI_BWD) ? 2 : ok(4, EPI_BWD) ? 4 : 1;
 #ifdef FNO_DEV_KNOBS   // development builds only: FNO_PASS_C_FAM=<u><fwd><bwd> digits force families
   if (const char* fe = std::getenv("FNO_PASS_C_FAM")) {
     for (int m = 0; m < 3 && fe[m]; ++m) {
       const int f = fe[m] - '0';
-      if (f >= 1 && f <= 4 && ok(f, m)) p->fam[m] = f;
+      if (f >= 1 && f <= 5 && ok(f, m)) p->fam[m] = f;
     }
   }
 #endif
@@ -381,6 +389,10 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
     return int(std::max<long long>(1, std::min<long long>(n_cols, (long long)p->num_sms * per_sm)));
   };
   p->max_grid_c = 1;
+  if (p->C <= 20) {
+    p->dw_grid = dw_partial_grid(p->B, p->Xl * p->Yl * p->Z * p->T, p->num_sms);
+    p->max_grid_c = std::max(p->max_grid_c, p->dw_grid);
+  }
   for (int f = 0; f < 4; ++f)
     for (int m = 0; m < 3; ++m) {
       fno_plan_s::KCfg& g = p->kc[f][m];
@@ -538,16 +550,17 @@ extern "C" fno_status fno_plan_pass_c_info(fno_plan_t p, int mode, int64_t info[
   if (!p || !info || mode < 0 || mode > 2) return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_pass_c_info: bad arguments");
   const int m = mode == 0 ? EPI_U : (mode == 1 ? EPI_FWD : EPI_BWD);
   const int f = p->fam[m];
-  const auto& g = p->kc[f - 1][m];
+  // family 5: the configuration of its dv kernel (the forward family's)
+  const auto& g = f == 5 ? p->kc[p->fam[EPI_FWD] - 1][EPI_FWD] : p->kc[f - 1][m];
   info[0] = f; info[1] = g.cp; info[2] = g.nx; info[3] = int64_t(g.smem);
   return FNO_OK;
 }
 
 extern "C" fno_status fno_plan_set_pass_c(fno_plan_t p, int mode, int family) {
-  if (!p || mode < 0 || mode > 2 || family < 1 || family > 4)
-    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_pass_c: mode 0..2, family 1..4");
+  if (!p || mode < 0 || mode > 2 || family < 1 || family > 5)
+    return fail(FNO_ERR_INVALID_ARGUMENT, "fno_plan_set_pass_c: mode 0..2, family 1..5");
   const int m = mode == 0 ? EPI_U : (mode == 1 ? EPI_FWD : EPI_BWD);
-  if (p->kc[family - 1][m].cp == 0)
+  if (family == 5 ? (m != EPI_BWD || p->dw_grid == 0) : p->kc[family - 1][m].cp == 0)
     return fail(FNO_ERR_PLAN, "fno_plan_set_pass_c: that pass C kernel family does not cover this problem");
   p->fam[m] = family;
   return FNO_OK;
@@ -880,16 +893,29 @@ fno_status stage_c_fwd(fno_plan_t p, const float* v, const float* W, const float
 // into dW / db when loc is NULL)
 fno_status stage_c_bwd(fno_plan_t p, const float* v, const float* dz, const float* W, float* dv, float* loc, float* dW,
                        float* db, int accumulate, cudaStream_t st) {
-  PassCParams c = make_c(p, EPI_BWD);
-  c.v = v; c.dy = dz; c.W = W; c.out = dv;
-  c.dWpart = wsp<float>(p, p->o_dwpart);
   int nparts = 1;
-  FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, st, &nparts), "pass C (layer backward)");
+  if (p->fam[EPI_BWD] == 5) {
+    // split backward: dv = W^T dz + S^T dz by the forward-mode kernel (the
+    // contraction with W^T, no bias, identity, no z), then dW / db from dz, v
+    PassCParams c = make_c(p, EPI_FWD);
+    c.v = dz; c.W = W; c.w_t = 1; c.bias = nullptr; c.act_gelu = 0; c.zsave = nullptr; c.out = dv;
+    FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_FWD, st), "pass C (layer backward, dv)");
+    DwParams d{};
+    d.dz = dz; d.v = v; d.part = wsp<float>(p, p->o_dwpart);
+    d.N = p->Xl * p->Yl * p->Z * p->T; d.B = p->B; d.C = p->C;
+    FNO_LAUNCH(p, ST_DWP, launch_dw_partial(d, p->dw_grid, st), "dW/db partials");
+    nparts = p->dw_grid;
+  } else {
+    PassCParams c = make_c(p, EPI_BWD);
+    c.v = v; c.dy = dz; c.W = W; c.out = dv;
+    FNO_LAUNCH(p, ST_PASS_C, run_pass_c(p, c, EPI_BWD, st, &nparts), "pass C (layer backward)");
+  }
+  const float* dWpart = wsp<float>(p, p->o_dwpart);
   const int len = p->C * p->C + p->C;
   if (!loc) {
-    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, nparts, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(dWpart, nparts, len, p->C * p->C, dW, db, accumulate, st), "dW/db reduction");
   } else {
-    FNO_LAUNCH(p, ST_DW, launch_rowsum(c.dWpart, nparts, len, len, loc, nullptr, 0, st), "dW/db local reduction");
+    FNO_LAUNCH(p, ST_DW, launch_rowsum(dWpart, nparts, len, len, loc, nullptr, 0, st), "dW/db local reduction");
   }
   return FNO_OK;
 }

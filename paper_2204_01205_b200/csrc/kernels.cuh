@@ -82,6 +82,7 @@ struct PassCParams {
   unsigned long long* prof;   // development builds (FNO_C4_PROFILE): pass_c4 role timers, [grid][16]
   int ablate;           // profiling only (FNO_ABLATE): bit 0 skip phase 2, bit 1 skip 1x1, bit 2 skip stores, bit 3 skip dW, bit 4 skip phase 1
   int act_gelu;         // 1: sigma = GELU, 0: identity
+  int w_t;              // EPI_FWD kernels: contract with W^T (the dv = W^T dz leg of the split backward)
   float inv_n;          // 1 / (X Y Z T)
   KzSlab slab;
 };

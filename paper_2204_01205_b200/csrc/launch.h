@@ -66,6 +66,21 @@ cudaError_t launch_b_yinv(const PassBParams& p, int L, cudaStream_t st);
 cudaError_t launch_mix_fwd(const MixParams& p, cudaStream_t st);
 cudaError_t launch_mix_bwd(const MixParams& p, cudaStream_t st);
 
+// dW / db partials of the split backward (dw.cu): per CTA one row
+// [C * C + C] of sum_b sum_n dz[b][o][n] v[b][i][n] and sum dz[b][o][n], n over the
+// N = Xl Yl Z T points of a channel (NCXYZT fields); C <= 20
+struct DwParams {
+  const float* dz;
+  const float* v;
+  float* part;          // [grid][C * C + C]
+  long long N;
+  int B, C;
+  int bulk;             // set by launch_dw_partial: rows 16-byte aligned (2-D TMA tiles), else plain loads
+};
+size_t dw_partial_smem(int C);
+int dw_partial_grid(int B, long long N, int num_sms);
+cudaError_t launch_dw_partial(const DwParams& p, int grid, cudaStream_t st);
+
 // deterministic fixed-order sum of nparts rows of `len` floats; columns
 // [0, split) go to out0, the rest to out1 (nullable); out = sum or out += sum
 cudaError_t launch_rowsum(const float* parts, int nparts, int len, int split, float* out0, float* out1, int accumulate,

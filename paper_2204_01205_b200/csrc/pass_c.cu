@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(CT, 1) pass_c_kernel(PassCParams p) {
     for (int e = tid; e < C * Cp; e += nt) {
       const int k = e / Cp, o = e - k * Cp;
       float w = 0.f;
-      if (o < C) w = (EPI == EPI_FWD) ? p.W[o * C + k] : p.W[k * C + o];
+      if (o < C) w = (EPI == EPI_FWD && !p.w_t) ? p.W[o * C + k] : p.W[k * C + o];
       Ws[e] = w;
     }
     for (int o = tid; o < C; o += nt) bs[o] = (EPI == EPI_FWD && p.bias) ? p.bias[o] : 0.f;

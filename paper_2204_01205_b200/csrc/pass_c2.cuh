@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(C2T, EPI == EPI_FWD ? 3 : 2) pass_c2_kernel(co
     const int q = r / QW, j = r - q * QW;
     const int o = q * Q4 + j;
     float w = 0.f;
-    if (j < Q4 && o < C && k < C) w = (EPI == EPI_FWD) ? p.W[o * C + k] : p.W[k * C + o];
+    if (j < Q4 && o < C && k < C) w = (EPI == EPI_FWD && !p.w_t) ? p.W[o * C + k] : p.W[k * C + o];
     Ws[e] = w;
   }
   for (int o = tid; o < CP; o += C2T) bs[o] = (EPI == EPI_FWD && p.bias && o < C) ? p.bias[o] : 0.f;

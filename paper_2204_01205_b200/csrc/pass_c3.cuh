@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
     const int o = e / KP, k = e - o * KP;
     float w = 0.f;
     if (o < C) {
-      if (k < C) w = p.W[o * C + k];
+      if (k < C) w = p.w_t ? p.W[k * C + o] : p.W[o * C + k];
       else if (k == CP && p.bias) w = p.bias[o];
     }
     const float hi = tf32_hi(w);

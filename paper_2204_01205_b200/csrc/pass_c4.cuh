@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(C4T, 1) pass_c4_kernel(const __grid_constant__
       const int n = e / KP, k = e - n * KP;
       float w = 0.f;
       if (n < C) {
-        if (k < C) w = BWD ? p.W[k * C + n] : p.W[n * C + k];
+        if (k < C) w = (BWD || p.w_t) ? p.W[k * C + n] : p.W[n * C + k];
         else if (!BWD && k == CP && p.bias) w = p.bias[n];
       }
       const float hi = tf32_hi(w);

@@ -40,7 +40,7 @@ def timeit(fn, n=10):
 
 
 for mode in ("fwd", "bwd"):
-    for fam in (2, 3, 4):
+    for fam in ((2, 3, 4) if mode == "fwd" else (2, 4, 5)):
         try:
             fno.plan_set_pass_c(plan, mode, fam)
         except fno.FnoError:
@@ -54,4 +54,7 @@ for mode in ("fwd", "bwd"):
         pr = plan.profile_read()
         plan.profile_enable(False)
         k = f"{mode}.pass_c"
-        print(f"c{ci} {mode} family {fam}: layer {t:.3f} ms, pass C {pr[k][0] / pr[k][1]:.3f} ms/launch")
+        extra = ""
+        if mode == "bwd" and fam == 5 and "bwd.dw" in pr:
+            extra = f", dw_partial {pr['bwd.dw'][0] / pr['bwd.dw'][1]:.3f} ms/launch"
+        print(f"c{ci} {mode} family {fam}: layer {t:.3f} ms, pass C {pr[k][0] / pr[k][1]:.3f} ms/launch{extra}")

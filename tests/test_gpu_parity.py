@@ -340,7 +340,7 @@ FAMILY_CASES = [
 ]
 
 
-@pytest.mark.parametrize("family", [2, 3, 4])
+@pytest.mark.parametrize("family", [2, 3, 4, 5])
 @pytest.mark.parametrize("case", FAMILY_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_C{c[1]}")
 def test_pass_c_families_fwd_bwd(case, family):
     import torch
@@ -373,6 +373,60 @@ def test_pass_c_families_fwd_bwd(case, family):
     dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
     for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
         assert rel_l2(G.np64(got), ref) < TOL, (name, rel_l2(G.np64(got), ref))
+
+
+# The split backward (family 5) with each forward kernel as its dv leg (the
+# contraction with W^T: w_t), on the FAMILY_CASES shapes plus a batch of 2, an
+# odd width, and a v that is not 16-byte aligned (dw_partial's plain-load path;
+# Xl Yl Z T is a multiple of 4 for every instantiated transform size, so only a
+# misaligned base pointer takes it).
+SPLIT_CASES = [c + (1, False) for c in FAMILY_CASES] + [
+    ((16, 16, 16, 8), 6, (4, 4, 4, 4), 2, False),
+    ((12, 10, 12, 10), 3, (3, 2, 3, 3), 2, True),
+    ((32, 32, 64, 30), 20, (12, 12, 12, 12), 1, True),
+]
+
+
+@pytest.mark.parametrize("fwd_family", [2, 3, 4])
+@pytest.mark.parametrize("case", SPLIT_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_C{c[1]}_B{c[3]}"
+                         + ("_misaligned" if c[4] else ""))
+def test_split_backward_dv_kernels(case, fwd_family):
+    import torch
+    from tests import _gpu as G
+    import paper_2204_01205_b200 as fno
+    grid, C, modes, B, misalign = case
+    v, R, W, b, dy = _problem(grid, C, modes, B, seed=717)
+    plan = G.make_plan(grid, C, modes, B)
+    try:
+        fno.plan_set_pass_c(plan, "fwd", fwd_family)
+        fno.plan_set_pass_c(plan, "bwd", 5)
+    except fno.FnoError:
+        pytest.skip(f"forward family {fwd_family} does not cover this shape")
+    info = fno.plan_pass_c_kernels(plan)
+    assert info["bwd"]["family"].startswith("split") and info["bwd"]["dv_kernel"] == info["fwd"]["family"]
+    y, z, vh = G.layer_fwd(plan, v, R, W, b)
+    dyt = G.t32(dy)
+    dv = torch.empty_like(dyt)
+    dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
+    dW = torch.full((C, C), 7.0, device="cuda")
+    db = torch.full((C,), 7.0, device="cuda")
+    vt = G.t32(v)
+    if misalign:   # the same values one float past a 16-byte boundary
+        buf = torch.empty(vt.numel() + 1, device="cuda")
+        vt = buf[1:].view(vt.shape)
+        vt.copy_(G.t32(v))
+        assert vt.data_ptr() % 16 != 0
+    fno.layer_bwd(plan, vt, z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW, db)
+    torch.cuda.synchronize()
+    dv_r, dR_r, dW_r, db_r = sp.layer_bwd(G.f32(v), G.f32(dy), G.f32(R), G.f32(W), G.f32(b), modes)
+    for name, got, ref in (("dv", dv, dv_r), ("dR", dR, dR_r), ("dW", dW, dW_r), ("db", db, db_r)):
+        assert rel_l2(G.np64(got), ref) < TOL, (name, rel_l2(G.np64(got), ref))
+    # accumulate = 1 adds into dW / db
+    dW2, db2 = dW.clone(), db.clone()
+    fno.layer_bwd(plan, vt, z, vh, dyt, G.tc64(R), G.t32(W), dv, dR, dW2, db2, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_l2(G.np64(dW2), 2 * dW_r) < TOL and rel_l2(G.np64(db2), 2 * db_r) < TOL
+    plan.destroy()
 
 
 # Batched mixing: B > 1 reads R once per mode for all batch
