@@ -88,18 +88,26 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
-    def _run(self):
+    def sample_once(self):
+        """One SM-clock / throttle-reason reading per GPU (also called from the
+        timing loop after every repetition, so short timed regions are covered
+        even when the sampling thread is starved)"""
         nv = self.nv
+        if nv is None:
+            return
+        for h in self.handles:
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+
+    def _run(self):
         while not self._stop.is_set():
-            for h in self.handles:
-                try:
-                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    for bit, name in self.REASONS.items():
-                        if r & bit and name != "gpu_idle":
-                            self.reasons.add(name)
-                except Exception:
-                    pass
+            self.sample_once()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -389,7 +397,7 @@ def run_ours(args, rank, world, local_rank):
 
     run, per_step = as_graph(step)
 
-    def timed(fn, reps):
+    def timed(fn, reps, sampler=None):
         """Per-repetition device times (ms): a barrier before each repetition,
         CUDA events on the launching stream, then the max over ranks."""
         ts = []
@@ -399,6 +407,8 @@ def run_ours(args, rank, world, local_rank):
             e0.record(stream)
             fn()
             e1.record(stream)
+            if sampler is not None:   # the GPU is still running this repetition
+                sampler.sample_once()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
         t = torch.tensor(ts, dtype=torch.float64, device=dev)
@@ -410,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
     n0 = fno.kernel_launches()
     sampler = ClockSampler([nvml_index(local_rank)])
     with sampler:
-        step_ms = timed(run, args.steps)
+        step_ms = timed(run, args.steps, sampler)
         barrier()
     launches = per_step * args.steps if use_graph else fno.kernel_launches() - n0
     ms_step = float(statistics.median(step_ms))

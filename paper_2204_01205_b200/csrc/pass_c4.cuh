@@ -120,7 +120,9 @@ __host__ __device__ inline C4Layout c4_layout(int CP, int mode, int C, int Z, in
   L.b1hi = take(size_t(L.NP) * L.KP * sizeof(float));
   L.b1lo = take(size_t(L.NP) * L.KP * sizeof(float));
   L.bb = take(size_t(C) * L.nk * L.TP * sizeof(float2));
-  L.ustride = (size_t(C) * L.UPS * sizeof(float) + 1023) & ~size_t(1023);
+  // U buffers only need 16-byte rows: 128-byte granules (c3 forward: four U
+  // buffers next to the staged slab then fit 227 KB)
+  L.ustride = (size_t(C) * L.UPS * sizeof(float) + 127) & ~size_t(127);
   L.u0 = take(L.ustride * NUB);
   L.sl = take(SL ? size_t(C) * 2 * mz * mt * sizeof(float2) : 0);
   auto take16 = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
