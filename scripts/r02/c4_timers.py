@@ -22,10 +22,14 @@ W, b = [torch.from_numpy(a).cuda() for a in synth.channel_weights(C, 3)]
 y, z = torch.empty_like(v), torch.empty_like(v)
 vh = torch.empty(plan.vhat_shape(), dtype=torch.complex64, device="cuda")
 mode = sys.argv[2] if len(sys.argv) > 2 else "fwd"
-fno.plan_set_pass_c(plan, mode, 4)
+if mode == "dv":   # the split backward's dv leg: the forward pass_c4 with W^T
+    fno.plan_set_pass_c(plan, "fwd", 4)
+    fno.plan_set_pass_c(plan, "bwd", 5)
+else:
+    fno.plan_set_pass_c(plan, mode, 4)
 for _ in range(3):
     fno.layer_fwd(plan, v, R, W, b, y, z, vh)
-if mode == "bwd":
+if mode in ("bwd", "dv"):
     dv = torch.empty_like(v)
     dR = torch.empty(plan.weight_shape(), dtype=torch.complex64, device="cuda")
     dW = torch.empty((C, C), device="cuda")
