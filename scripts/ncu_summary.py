@@ -40,7 +40,26 @@ def stage_of(name):
         return "fwd.mix"
     if base == "mix_bwd_kernel":
         return "bwd.mix"
+    if base == "dw_partial_kernel":
+        return "bwd.dw"
     return base
+
+
+def stages_in_order(names):
+    """stage_of over a launch sequence: a forward-mode pass C that follows a
+    backward pass A is the split backward's dv leg (pass C family 5: the forward
+    kernel run with W^T), i.e. bwd.pass_c"""
+    out, in_bwd = [], False
+    for n in names:
+        st = stage_of(n)
+        if st == "bwd.pass_a":
+            in_bwd = True
+        elif st == "fwd.pass_a":
+            in_bwd = False
+        if st == "fwd.pass_c" and in_bwd:
+            st = "bwd.pass_c"
+        out.append(st)
+    return out
 
 
 def num(x):
@@ -77,7 +96,8 @@ def summarise_rep(rep):
     rows, units = raw_rows(rep)
     stall_keys = [k for k in rows[0] if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued")]
     res = []
-    for r in rows:
+    stages = stages_in_order([r.get("Kernel Name", "") for r in rows])
+    for r, stage in zip(rows, stages):
         name = r.get("Kernel Name", "")
         rd = to_bytes(r["dram__bytes_read.sum"], units["dram__bytes_read.sum"])
         wr = to_bytes(r["dram__bytes_write.sum"], units["dram__bytes_write.sum"])
@@ -85,7 +105,7 @@ def summarise_rep(rep):
         st = sorted(((num(r[k]), k.replace("smsp__pcsamp_warps_issue_stalled_", "")) for k in stall_keys), reverse=True)
         tot = sum(v for v, _ in st if v == v) or 1.0
         res.append(dict(
-            kernel=name[:160], stage=stage_of(name), duration_us=round(us, 2),
+            kernel=name[:160], stage=stage, duration_us=round(us, 2),
             dram_read_bytes=int(rd), dram_write_bytes=int(wr), dram_bytes=int(rd + wr),
             dram_gbs=round((rd + wr) / (us * 1e-6) / 1e9, 1) if us > 0 else None,
             dram_pct_peak=num(r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "nan")),
@@ -108,11 +128,9 @@ def summarise_launches(path):
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
     rows = list(csv.DictReader(lines[start:]))
     fam = collections.OrderedDict()
-    for r in rows:
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+    rows = [r for r in rows if r.get("Metric Name") == "gpu__time_duration.sum"]
+    for r, st in zip(rows, stages_in_order([r["Kernel Name"] for r in rows])):
         us = to_us(r["Metric Value"], r["Metric Unit"])
-        st = stage_of(r["Kernel Name"])
         f = fam.setdefault(st, [0, 0.0])
         f[0] += 1
         f[1] += us

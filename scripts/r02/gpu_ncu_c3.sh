@@ -4,7 +4,7 @@
 set -u
 O=gpurun_out/r02; mkdir -p $O
 CMD="python bench.py --config c3 --steps 2 --warmup 1 --layers 1 --no-cpu-baseline --no-phases --no-graph"
-K='regex:pass_|b_[xy]|mix_|rowsum'
+K='regex:pass_|b_[xy]|mix_|rowsum|dw_'
 $CMD > $O/plain_c3.log 2>&1; echo "plain rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -s 15 -c 30 --csv --log-file $O/launches_c3.csv $CMD > $O/ncu_launch_c3.log 2>&1; echo "ncu launches rc=$?"
 timeout 1500 ncu --set full --clock-control none --import-source on -k "$K" -s 15 -c 15 -o $O/prof_c3_full $CMD > $O/ncu_full_c3.log 2>&1; echo "ncu full rc=$?"

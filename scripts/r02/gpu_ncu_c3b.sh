@@ -5,8 +5,8 @@ set -u
 O=gpurun_out/r02c3; mkdir -p $O
 CMD="python bench.py --config c3 --steps 2 --warmup 1 --layers 1 --no-cpu-baseline --no-phases --no-graph"
 $CMD > $O/plain_c3.log 2>&1; echo "plain rc=$?"
-ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:pass_|b_[xy]|mix_|rowsum' -s 15 -c 30 --csv --log-file $O/launches_c3.csv $CMD > $O/ncu_launch_c3.log 2>&1; echo "ncu launches rc=$?"
-timeout 1500 ncu --set full --clock-control none -k 'regex:pass_|mix_|b_[xy]|rowsum' -s 15 -c 15 -o /tmp/prof_c3_full $CMD > $O/ncu_full_c3.log 2>&1; echo "ncu full rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:pass_|b_[xy]|mix_|rowsum|dw_' -s 16 -c 32 --csv --log-file $O/launches_c3.csv $CMD > $O/ncu_launch_c3.log 2>&1; echo "ncu launches rc=$?"
+timeout 1500 ncu --set full --clock-control none -k 'regex:pass_|mix_|b_[xy]|rowsum|dw_' -s 16 -c 16 -o /tmp/prof_c3_full $CMD > $O/ncu_full_c3.log 2>&1; echo "ncu full rc=$?"
 ncu -i /tmp/prof_c3_full.ncu-rep --page raw --csv > $O/prof_c3_raw.csv 2>&1
 ncu -i /tmp/prof_c3_full.ncu-rep --page details --csv > $O/prof_c3_details.csv 2>&1
 gzip -f $O/prof_c3_raw.csv $O/prof_c3_details.csv
