@@ -380,7 +380,7 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
   const long long n_planes = (long long)p->B * p->C * p->Xl * p->Yl;
   for (int m = 0; m < 3; ++m) {
     const long long n_batches = (n_planes + p->np_a[m] - 1) / p->np_a[m];
-    const int per_sm_a = std::max(1, int(std::min<size_t>(8, (228 * 1024) / (p->smem_a[m] + 1024))));
+    const int per_sm_a = std::max(1, int(std::min<size_t>(pass_a_max_blocks(m, int(p->T)), (228 * 1024) / (p->smem_a[m] + 1024))));
     p->grid_a_m[m] = int(std::max<long long>(1, std::min<long long>(n_batches, (long long)p->num_sms * per_sm_a)));
   }
   const long long n_cols = (long long)p->B * p->Xl * p->Yl;

@@ -28,6 +28,8 @@ namespace fno {
 
 // planes per batch NP, dynamic shared memory and TMA eligibility for a pass-A mode
 void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* smem, int* use_tma);
+int pass_a_threads(int mode, int T);      // threads per CTA of the mode's pass A kernel
+int pass_a_max_blocks(int mode, int T);   // its resident CTAs per SM (launch bounds)
 cudaError_t launch_pass_a(const PassAParams& p, int LZ, int LT, int mode, int grid, size_t smem, cudaStream_t st);
 
 

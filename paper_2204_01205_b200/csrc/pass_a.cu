@@ -25,6 +25,11 @@
 namespace fno {
 
 static constexpr int AT = 128;   // threads per CTA; several CTAs per SM overlap their phases
+static constexpr int AT5 = 160;  // forward, 128 % T != 0: floor(160 / T) planes make one phase-1 round (c3: 150 pencils)
+
+// threads per CTA and resident CTAs per SM (the launch bounds) of a mode's kernel
+int pass_a_threads(int mode, int T) { return (mode == MODE_V && 128 % T != 0 && T <= AT5) ? AT5 : AT; }
+int pass_a_max_blocks(int mode, int T) { return mode == MODE_V ? (pass_a_threads(mode, T) == AT ? 4 : 3) : 3; }
 
 struct ALayout {
   size_t stage[2], bb, twz, twt, dmap, jbase, jnk, bar, total;
@@ -54,8 +59,8 @@ __host__ __device__ inline ALayout a_layout(int Z, int T, int mz, int NP, int mo
 
 // HALF: mz = LZ / 2 (nk = LZ / 2 + 1 at compile time: the unused outputs of
 // the z codelet are dead code)
-template <int LZ, int LT, int MODE, bool HALF>
-__global__ void __launch_bounds__(AT, MODE == MODE_V ? 4 : 3) pass_a_kernel(PassAParams p) {
+template <int LZ, int LT, int MODE, bool HALF, int NT = AT>
+__global__ void __launch_bounds__(NT, MODE == MODE_V ? (NT == AT ? 4 : 3) : 3) pass_a_kernel(PassAParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Z = p.Z, T = p.T, mz = p.mz, mt = p.mt;
   const int ZT = Z * T;
@@ -251,7 +256,10 @@ void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* sme
   // (backward, two input arrays: floor, np0 T <= 128 pencils = one per thread,
   // e.g. T = 30 -> 4 planes, 120 pencils in one round instead of 150 in two:
   // c3 backward 0.53 -> 0.39 ms; the forward keeps ceil, measured 0.25 vs 0.275 ms)
-  const int np0 = std::max(1, mode == MODE_DZ_GELU ? AT / T : (AT + T - 1) / T);
+  // (forward with 128 % T != 0: 160 threads and floor(160 / T) planes, one
+  // phase-1 round, three CTAs per SM; c3 0.249 -> 0.242 ms, bench_c3_a160.json)
+  const int at = pass_a_threads(mode, T);
+  const int np0 = std::max(1, mode == MODE_DZ_GELU || at != AT ? at / T : (AT + T - 1) / T);
   const size_t per3 = 75 * 1024, per2 = 113 * 1024;
   const int cand[4][2] = {{np0, 2}, {np0, 1}, {std::max(1, np0 / 2), 2}, {std::max(1, np0 / 2), 1}};
   const size_t lim[4] = {per3, per2, per3, per3};
@@ -285,13 +293,15 @@ void pass_a_config(int Z, int T, int mz, int mode, int* NP, int* NS, size_t* sme
 template <int LZ, int LT>
 static cudaError_t launch_a(const PassAParams& p, int mode, int grid, size_t smem, cudaStream_t st) {
   const bool half = 2 * p.mz == LZ;
+  const int nt = pass_a_threads(mode, p.T);
   void (*k)(PassAParams) =
-      mode == MODE_V ? (half ? pass_a_kernel<LZ, LT, MODE_V, true> : pass_a_kernel<LZ, LT, MODE_V, false>)
+      mode == MODE_V ? (nt == AT5 ? (half ? pass_a_kernel<LZ, LT, MODE_V, true, AT5> : pass_a_kernel<LZ, LT, MODE_V, false, AT5>)
+                                  : (half ? pass_a_kernel<LZ, LT, MODE_V, true> : pass_a_kernel<LZ, LT, MODE_V, false>))
       : mode == MODE_DZ_GELU ? (half ? pass_a_kernel<LZ, LT, MODE_DZ_GELU, true> : pass_a_kernel<LZ, LT, MODE_DZ_GELU, false>)
                              : (half ? pass_a_kernel<LZ, LT, MODE_DZ_NONE, true> : pass_a_kernel<LZ, LT, MODE_DZ_NONE, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  k<<<grid, AT, smem, st>>>(p);
+  k<<<grid, nt, smem, st>>>(p);
   return cudaGetLastError();
 }
 
