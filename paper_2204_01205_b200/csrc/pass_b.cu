@@ -16,13 +16,14 @@
 namespace fno {
 
 static constexpr int BT = 128;  // threads per CTA of the pencil kernels
-// The forward pencils run at <= 128 registers (four CTAs per SM, a few spilled
-// registers): c3 y forward 0.067 -> 0.065, x forward 0.032 -> 0.028 ms/launch;
-// the inverse ones lost with it and keep the compiler's allocation
+// The forward pencils of length >= 30 run at <= 128 registers (four CTAs per
+// SM, a few spilled registers): c3 (L = 32) y forward 0.067 -> 0.065, x forward
+// 0.032 -> 0.028 ms/launch; at c2 (L = 16) the y forward lost with it (0.027 ->
+// 0.031), as did the inverse pencils: they keep the compiler's allocation
 
 // y forward: slab (x/y-source ordered) -> H.  pencil = (b, kzl, c, x, kt)
 template <int L>
-__global__ void __launch_bounds__(BT, 4) b_yfwd_kernel(PassBParams p) {
+__global__ void __launch_bounds__(BT, L >= 30 ? 4 : 1) b_yfwd_kernel(PassBParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);               // Y
   long long* ypart = reinterpret_cast<long long*>(tw + p.Y);      // Y
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(BT, 4) b_yfwd_kernel(PassBParams p) {
 
 // x forward: H -> V^.  pencil = (b, kzl, c, jy, kt)
 template <int L>
-__global__ void __launch_bounds__(BT, 4) b_xfwd_kernel(PassBParams p) {
+__global__ void __launch_bounds__(BT, L >= 30 ? 4 : 1) b_xfwd_kernel(PassBParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* tw = reinterpret_cast<float2*>(smem_raw);
   fill_combine_table(tw, L, p.Q, p.X, p.mx, -1, threadIdx.x, blockDim.x);
