@@ -9,8 +9,12 @@ import sys
 rep = sys.argv[1]
 ksub = sys.argv[2] if len(sys.argv) > 2 else ""
 N = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv") or rep.endswith(".csv.gz"):   # the source page exported on the GPU box
+    import gzip
+    out = (gzip.open(rep, "rt") if rep.endswith(".gz") else open(rep)).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 per = {}
 fpath = func = None
