@@ -397,22 +397,16 @@ __global__ void __launch_bounds__(c3_threads(CP, LZ), 2) pass_c3_fwd_kernel(cons
           if (o >= C || FNO_ABL(p, 4) || k0 >= k1) break;
           float4 r = *reinterpret_cast<const float4*>(U + o * UPS + pq);
           const long long g = gq + o * chan_stride;
-          if (v4) {
-            if (p.zsave) __stcs(reinterpret_cast<float4*>(p.zsave + g), r);
-            if (p.act_gelu) {
-              r.x = gelu_f(r.x); r.y = gelu_f(r.y); r.z = gelu_f(r.z); r.w = gelu_f(r.w);
-            }
-            __stcs(reinterpret_cast<float4*>(p.out + g), r);
-          } else {
-            const float rv[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              if (kk >= k0 && kk < k1) {
-                if (p.zsave) p.zsave[g + kk] = rv[kk];
-                p.out[g + kk] = p.act_gelu ? gelu_f(rv[kk]) : rv[kk];
-              }
-            }
+          // one copy of the GELU for the full-quad and the ragged stores (code size)
+          if (p.zsave) {
+            if (v4) __stcs(reinterpret_cast<float4*>(p.zsave + g), r);
+            else store_quad_part(p.zsave + g, r, k0, k1);
           }
+          if (p.act_gelu) {
+            r.x = gelu_f(r.x); r.y = gelu_f(r.y); r.z = gelu_f(r.z); r.w = gelu_f(r.w);
+          }
+          if (v4) __stcs(reinterpret_cast<float4*>(p.out + g), r);
+          else store_quad_part(p.out + g, r, k0, k1);
         }
         mbar_arrive(&bempty[b]);   // U[b], D[b] free
       }

@@ -46,7 +46,7 @@ bool pass_c4_config(int C, int Z, int T, int mz, int mt, int LZ, int mode, int* 
   struct Pref { int sl, nub, nsmin; };
   const Pref prefs[] = {{1, 4, 3}, {1, 4, 2}, {1, 2, 3}, {0, 4, 3}, {0, 2, 2}};
   for (const Pref& pr : prefs) {
-    if (pr.sl && !sl_ok) continue;
+    if (pr.sl && (!sl_ok || mode == EPI_BWD)) continue;   // (the backward kernels are built without the staged slab)
     for (int ns = mode == EPI_FWD ? C4_MAXNS : 4; ns >= pr.nsmin; --ns) {
       const size_t s = c4_layout(CP, mode, C, Z, T, mz, LZ, ns, pr.nub, pr.sl, mt).total;
       if (s <= cap) {
