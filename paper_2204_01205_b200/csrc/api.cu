@@ -348,19 +348,17 @@ extern "C" fno_status fno_plan_create(const fno_problem* pb, fno_comm_t comm, fn
       h.cp = cp; h.tch = 128 / p->LZ; h.nx = ns; h.smem = sm;
     }
   }
-  // default choice, by measurement on B200 (profiles/r02/ab_pass_c.md): the
-  // spectral u path on pass_c4; the layer forward on pass_c3 where it tiles T
-  // (T % 4 == 0), else pass_c4 (c3: 1.28 vs 1.37 ms); the layer backward split
-  // (family 5: dv by the forward kernel, dW / db by dw_partial) where T % 4 != 0,
-  // whose ragged t chunks cost the fused pass_c2 backward a zero fill of both
-  // tiles per chunk (c3: 1.94 vs 2.08 ms per layer backward), else the FFMA
-  // pass_c2 (c2: 1.31 vs 1.33, c4: 5.59 vs 5.67 ms split; 0.80 vs 2.05 ms for
-  // the tcgen05 pass_c4 backward, whose three operand splits and
-  // single-buffered operands serialise the tile pipeline)
+  // default choice, by measurement on B200 (profiles/r02/ab_pass_c.md, after the
+  // pass_c4 code-size cut): the spectral u path and the layer forward on pass_c4
+  // (c2 0.945 vs 0.960 ms per layer forward with pass_c3, c4 3.99 vs 4.11 with
+  // pass_c2); the layer backward split (family 5: dv by the forward kernel, dW / db
+  // by dw_partial; c2 1.29 vs 1.31, c3 1.94 vs 2.08, c4 5.50 vs 5.58 ms per layer
+  // backward against the fused FFMA pass_c2; the tcgen05 pass_c4 backward, 2.05 ms
+  // at c2, serialises its three operand splits)
   auto ok = [&](int f, int m) { return f == 5 ? (m == EPI_BWD && p->C <= 20) : p->kc[f - 1][m].cp > 0; };
   p->fam[EPI_U] = ok(4, EPI_U) ? 4 : 1;
-  p->fam[EPI_FWD] = (ok(3, EPI_FWD) && p->T % 4 == 0) ? 3 : ok(4, EPI_FWD) ? 4 : ok(3, EPI_FWD) ? 3 : ok(2, EPI_FWD) ? 2 : 1;
-  p->fam[EPI_BWD] = (ok(5, EPI_BWD) && p->T % 4 != 0) ? 5 : ok(2, EPI_BWD) ? 2 : ok(4, EPI_BWD) ? 4 : 1;
+  p->fam[EPI_FWD] = ok(4, EPI_FWD) ? 4 : ok(3, EPI_FWD) ? 3 : ok(2, EPI_FWD) ? 2 : 1;
+  p->fam[EPI_BWD] = ok(5, EPI_BWD) ? 5 : ok(2, EPI_BWD) ? 2 : ok(4, EPI_BWD) ? 4 : 1;
 #ifdef FNO_DEV_KNOBS   // development builds only: FNO_PASS_C_FAM=<u><fwd><bwd> digits force families
   if (const char* fe = std::getenv("FNO_PASS_C_FAM")) {
     for (int m = 0; m < 3 && fe[m]; ++m) {

@@ -1,8 +1,8 @@
 """CPU tests of the host-side pass C kernel selection (api.cu fno_plan_create,
 pass_c4.cu pass_c4_config; no compute calls): the split backward (family 5:
 dv = W^T dz + S^T dz by the forward kernel, dW / db by dw_partial, the
-broadcast adjoint of P:64 / Eq. dist_block) is the default exactly where
-T % 4 != 0 and C <= 20, can be forced for the backward only, and bench.py's
+broadcast adjoint of P:64 / Eq. dist_block) is the default wherever
+C <= 20 (with pass_c4 as the forward), can be forced for the backward only, and bench.py's
 algorithmic bytes follow the family (the dv leg moves slab + dz +
 dv, dw_partial dz + v)."""
 
@@ -27,14 +27,13 @@ def _plan(grid, C, modes):
     return fno.Plan(fno.Problem(grid=grid, width=C, modes=modes), allocate=False)
 
 
-def test_split_backward_is_the_default_where_t_is_not_a_multiple_of_4(L):
-    c3 = _plan((64, 64, 64, 30), 20, (12, 12, 12, 12))   # BASELINE configs[2]
-    k = fno.plan_pass_c_kernels(c3)
-    assert k["bwd"]["family"].startswith("split")
-    assert k["bwd"]["dv_kernel"] == k["fwd"]["family"]
-    assert k["fwd"]["family"].startswith("pass_c4")
-    c2 = _plan((64, 64, 64, 32), 20, (8, 8, 8, 8))        # T % 4 == 0: the fused FFMA backward
-    assert fno.plan_pass_c_kernels(c2)["bwd"]["family"].startswith("pass_c2")
+def test_split_backward_and_pass_c4_are_the_defaults_up_to_width_20(L):
+    for grid, modes in (((64, 64, 64, 30), (12, 12, 12, 12)),    # BASELINE configs[2] (c3)
+                        ((64, 64, 64, 32), (8, 8, 8, 8))):       # configs[1] (c2)
+        k = fno.plan_pass_c_kernels(_plan(grid, 20, modes))
+        assert k["bwd"]["family"].startswith("split")
+        assert k["bwd"]["dv_kernel"] == k["fwd"]["family"]
+        assert k["fwd"]["family"].startswith("pass_c4")
 
 
 def test_split_backward_can_be_forced_and_is_backward_only(L):
